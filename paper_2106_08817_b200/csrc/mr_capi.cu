@@ -1,0 +1,403 @@
+// mr_capi.cu -- extern "C" boundary (include/morphreg_sm100.h) and the native
+// whole-loop drivers of shoot() / grad().
+//
+// The drivers replace the Python T-step loops of integrator.shoot
+// (integrator.py:163-219) and objective.grad (objective.py:91-174): one ctypes
+// call launches the whole forward sweep (2 kernels per step) or the whole
+// reverse sweep (memset + 2 kernels per step), stream-ordered, with no host
+// synchronisation inside.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mr_launch.cuh"
+
+namespace mr {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int check_cuda(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MR_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return MR_OK;
+}
+
+static int check_rc(int rc, const char* where) {
+  if (rc == MR_OK) return MR_OK;
+  if (rc < 0) {
+    cudaError_t e = cudaGetLastError();
+    return fail(rc, std::string(where) + ": " + cudaGetErrorString(e));
+  }
+  return fail(rc, std::string(where) + ": invalid argument");
+}
+
+static int validate(int dtype, const mr_grid& g) {
+  if (dtype != MR_F32 && dtype != MR_F64) return fail(MR_EINVAL, "dtype must be MR_F32 or MR_F64");
+  if (g.ndim != 2) return fail(MR_EINVAL, "only ndim == 2 is supported by this build");
+  if (g.batch < 1) return fail(MR_EINVAL, "batch must be >= 1");
+  if (g.n[0] < 2 || g.n[1] < 2)
+    return fail(MR_EINVAL, "grid must be at least 2x2, got " + std::to_string(g.n[0]) + "x" +
+                               std::to_string(g.n[1]));
+  if ((long long)g.n[0] * g.n[1] > (1LL << 31) - 1) return fail(MR_EINVAL, "grid too large");
+  return MR_OK;
+}
+
+static Grid2 grid2(const mr_grid& g) {
+  Grid2 r;
+  r.B = g.batch;
+  r.H = g.n[0];
+  r.W = g.n[1];
+  r.N = (long long)r.H * r.W;
+  return r;
+}
+
+template <typename T>
+static int make_taps(const mr_kernel& k, Taps<T>& tp) {
+  if (k.radius < 1 || k.radius > kMaxR)
+    return fail(MR_EINVAL, "kernel radius must lie in [1, " + std::to_string(kMaxR) + "], got " +
+                               std::to_string(k.radius));
+  if (!k.weights) return fail(MR_EINVAL, "kernel weights pointer is NULL");
+  const int R = k.radius;
+  std::memset(&tp, 0, sizeof(tp));
+  // symmetrise (the reference weights are exactly symmetric; this only guards
+  // against caller-side asymmetry since the transpose relies on it)
+  for (int t = 0; t <= 2 * R; ++t) {
+    double w = 0.5 * (k.weights[t] + k.weights[2 * R - t]);
+    if (!std::isfinite(w)) return fail(MR_EINVAL, "kernel weights must be finite");
+    tp.w[t] = (T)w;
+  }
+  double acc = 0.0;
+  for (int m = 0; m <= R; ++m) {  // W[m] = sum_{k<=m} w_k (kernel.py:48-68 edge rows)
+    acc += 0.5 * (k.weights[m] + k.weights[2 * R - m]);
+    tp.e[m] = (T)acc;
+  }
+  return MR_OK;
+}
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------------
+template <typename T>
+static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, const T* z,
+                            const T* v, T* In, T* zn, const T* phi_in, T* phi_out,
+                            cudaStream_t s) {
+  StepArgs<T> a{I, z, v, In, zn, phi_in, phi_out, (T)dt, (T)(dt * mu), mu != 0.0, g};
+  dim3 grid((g.W + 31) / 32, (g.H + kThreads / 32 - 1) / (kThreads / 32), g.B);
+  k_sl_step2d<T><<<grid, kThreads, 0, s>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I, const T* z,
+                               const T* v, const T* ibar, const T* zbar, T* ib, T* zb, T* vbar,
+                               cudaStream_t s) {
+  AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, g};
+  dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjTY - 1) / kAdjTY, g.B);
+  k_sl_adjoint2d<T><<<grid, kThreads, 0, s>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_cost_terms2d(const Grid2& g, double lam, double rho, const T* I0, const T* z0,
+                               const T* v0, const T* IT, const T* J, double* terms, T* seed,
+                               cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(terms, 0, sizeof(double) * 4 * g.B, s);
+  if (e != cudaSuccess) return MR_ECUDA;
+  CostArgs<T> a{I0, z0, v0, IT, J, seed, terms, g};
+  long long blocks = (g.N + kThreads * 4 - 1) / (kThreads * 4);
+  if (blocks > 1024) blocks = 1024;
+  k_cost_terms2d<T><<<dim3((unsigned)blocks, g.B), kThreads, 0, s>>>(a);
+  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, g.B, lam, rho);
+  return cuda_status(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------
+template <typename T>
+static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T_, void* trI,
+                         void* trz, void* trv, void* phi, int32_t* guard, cudaStream_t s) {
+  Taps<T> tp;
+  int rc = make_taps<T>(k, tp);
+  if (rc) return rc;
+  const Grid2 g = grid2(mg);
+  const double dt = 1.0 / T_;  // ShootingConfig.dt (integrator.py:67-69)
+  T* I = static_cast<T*>(trI);
+  T* z = static_cast<T*>(trz);
+  T* v = static_cast<T*>(trv);
+  const long long S1 = (long long)g.B * g.N;  // scalar state stride
+  const long long SV = 2 * S1;                 // vector state stride
+  T* ph[2] = {nullptr, nullptr};
+  if (phi) {
+    // phi holds 2 x [B][2][N]; the result ends in the first half.
+    T* base = static_cast<T*>(phi);
+    ph[0] = (T_ % 2 == 0) ? base : base + SV;
+    ph[1] = (T_ % 2 == 0) ? base + SV : base;
+    k_identity2d<T><<<592, 256, 0, s>>>(ph[0], g);
+  }
+  if (guard && cudaMemsetAsync(guard, 0, sizeof(int32_t) * (size_t)g.B * (T_ + 1), s) != cudaSuccess)
+    return check_cuda("memset guard");
+  for (int step = 0; step < T_; ++step) {
+    rc = launch_velocity2d<T>(g, k.radius, tp, I + step * S1, z + step * S1, v + step * SV,
+                              guard ? guard + step : nullptr, T_ + 1, s);
+    if (rc) return check_rc(rc, "velocity");
+    rc = launch_sl_step2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV,
+                             I + (step + 1) * S1, z + (step + 1) * S1, ph[step & 1],
+                             ph[(step + 1) & 1], s);
+    if (rc) return check_rc(rc, "sl_step");
+  }
+  rc = launch_velocity2d<T>(g, k.radius, tp, I + T_ * S1, z + T_ * S1, v + T_ * SV,
+                            guard ? guard + T_ : nullptr, T_ + 1, s);
+  if (rc) return check_rc(rc, "velocity");
+  return MR_OK;
+}
+
+template <typename T>
+static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T_, double lam,
+                         double rho, const void* trI, const void* trz, const void* trv,
+                         const void* Jv, void* zbar0, double* terms, int32_t* flags, void* ws,
+                         cudaStream_t s) {
+  Taps<T> tp;
+  int rc = make_taps<T>(k, tp);
+  if (rc) return rc;
+  const Grid2 g = grid2(mg);
+  const double dt = 1.0 / T_;
+  const T* I = static_cast<const T*>(trI);
+  const T* z = static_cast<const T*>(trz);
+  const T* v = static_cast<const T*>(trv);
+  const T* J = static_cast<const T*>(Jv);
+  const long long S1 = (long long)g.B * g.N;
+  const long long SV = 2 * S1;
+  T* w = static_cast<T*>(ws);
+  // workspace: [ibar, zbar] [ib_acc, zb_acc] vbar
+  T* cur = w;            // ibar | zbar   (2*S1)
+  T* acc = w + 2 * S1;   // ib   | zb     (2*S1)
+  T* vbar = w + 4 * S1;  // 2*S1
+  if (cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)g.B, s) != cudaSuccess)
+    return check_cuda("memset flags");
+  rc = launch_cost_terms2d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
+  if (rc) return check_rc(rc, "cost_terms");
+  if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
+  for (int step = T_ - 1; step >= 0; --step) {
+    if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
+    rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
+                                cur + S1, acc, acc + S1, vbar, s);
+    if (rc) return check_rc(rc, "sl_adjoint");
+    VelAdjArgs<T> a{};
+    a.I = I + step * S1;
+    a.z = z + step * S1;
+    a.vbar = vbar;
+    a.ib = acc;
+    a.zb = acc + S1;
+    a.g = g;
+    a.lam = (T)lam;
+    a.two_rho = (T)(2.0 * rho);
+    const bool reg = (step == 0);
+    if (reg) {
+      a.v0 = v;  // v at k = 0
+      a.zout = static_cast<T*>(zbar0);
+      a.flags = flags;
+    }
+    rc = launch_velocity_adj2d<T>(g, k.radius, tp, a, reg, s);
+    if (rc) return check_rc(rc, "velocity_adjoint");
+    T* t = cur;
+    cur = acc;
+    acc = t;
+  }
+  return MR_OK;
+}
+
+}  // namespace mr
+
+using namespace mr;
+
+// ================================ C ABI ===========================================
+extern "C" {
+
+int mr_version(void) { return 1; }
+
+const char* mr_last_error(void) { return g_last_error.c_str(); }
+
+const char* mr_strerror(int code) {
+  switch (code) {
+    case MR_OK: return "ok";
+    case MR_EINVAL: return "invalid argument";
+    case MR_ECUDA: return "CUDA error";
+    default: return "unknown error";
+  }
+}
+
+#define MR_DISPATCH(dtype, CALL_F32, CALL_F64) ((dtype) == MR_F32 ? (CALL_F32) : (CALL_F64))
+
+int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z, void* v,
+                int32_t* guard, void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!I || !z || !v) return fail(MR_EINVAL, "NULL field pointer");
+  Grid2 g2 = grid2(g);
+  if (dtype == MR_F32) {
+    Taps<float> tp;
+    if ((rc = make_taps<float>(k, tp))) return rc;
+    rc = launch_velocity2d<float>(g2, k.radius, tp, (const float*)I, (const float*)z, (float*)v,
+                                  guard, 1, as_stream(stream));
+  } else {
+    Taps<double> tp;
+    if ((rc = make_taps<double>(k, tp))) return rc;
+    rc = launch_velocity2d<double>(g2, k.radius, tp, (const double*)I, (const double*)z,
+                                   (double*)v, guard, 1, as_stream(stream));
+  }
+  return check_rc(rc, "mr_velocity");
+}
+
+int mr_smooth(int dtype, mr_grid g, mr_kernel k, const void* a, void* out, int32_t adjoint,
+              void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!a || !out) return fail(MR_EINVAL, "NULL field pointer");
+  Grid2 g2 = grid2(g);
+  if (dtype == MR_F32) {
+    Taps<float> tp;
+    if ((rc = make_taps<float>(k, tp))) return rc;
+    rc = launch_smooth2d<float>(g2, k.radius, tp, (const float*)a, (float*)out, adjoint != 0,
+                                as_stream(stream));
+  } else {
+    Taps<double> tp;
+    if ((rc = make_taps<double>(k, tp))) return rc;
+    rc = launch_smooth2d<double>(g2, k.radius, tp, (const double*)a, (double*)out, adjoint != 0,
+                                 as_stream(stream));
+  }
+  return check_rc(rc, "mr_smooth");
+}
+
+int mr_sl_step(int dtype, mr_grid g, double dt, double mu, const void* I, const void* z,
+               const void* v, void* I_next, void* z_next, const void* phi_in, void* phi_out,
+               void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!I || !z || !v || !I_next || !z_next) return fail(MR_EINVAL, "NULL field pointer");
+  if ((phi_in == nullptr) != (phi_out == nullptr))
+    return fail(MR_EINVAL, "phi_in and phi_out must both be set or both be NULL");
+  Grid2 g2 = grid2(g);
+  rc = MR_DISPATCH(dtype,
+                   launch_sl_step2d<float>(g2, dt, mu, (const float*)I, (const float*)z,
+                                           (const float*)v, (float*)I_next, (float*)z_next,
+                                           (const float*)phi_in, (float*)phi_out,
+                                           as_stream(stream)),
+                   launch_sl_step2d<double>(g2, dt, mu, (const double*)I, (const double*)z,
+                                            (const double*)v, (double*)I_next, (double*)z_next,
+                                            (const double*)phi_in, (double*)phi_out,
+                                            as_stream(stream)));
+  return check_rc(rc, "mr_sl_step");
+}
+
+int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu, const void* I, const void* z,
+                       const void* v, const void* ibar, const void* zbar, void* ib, void* zb,
+                       void* vbar, void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!I || !z || !v || !ibar || !zbar || !ib || !zb || !vbar)
+    return fail(MR_EINVAL, "NULL field pointer");
+  Grid2 g2 = grid2(g);
+  rc = MR_DISPATCH(
+      dtype,
+      launch_sl_adjoint2d<float>(g2, dt, mu, (const float*)I, (const float*)z, (const float*)v,
+                                 (const float*)ibar, (const float*)zbar, (float*)ib, (float*)zb,
+                                 (float*)vbar, as_stream(stream)),
+      launch_sl_adjoint2d<double>(g2, dt, mu, (const double*)I, (const double*)z,
+                                  (const double*)v, (const double*)ibar, (const double*)zbar,
+                                  (double*)ib, (double*)zb, (double*)vbar, as_stream(stream)));
+  return check_rc(rc, "mr_sl_step_adjoint");
+}
+
+int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
+                        const void* vbar, void* ib, void* zb, void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!I || !z || !vbar || !ib || !zb) return fail(MR_EINVAL, "NULL field pointer");
+  Grid2 g2 = grid2(g);
+  if (dtype == MR_F32) {
+    Taps<float> tp;
+    if ((rc = make_taps<float>(k, tp))) return rc;
+    VelAdjArgs<float> a{};
+    a.I = (const float*)I; a.z = (const float*)z; a.vbar = (const float*)vbar;
+    a.ib = (float*)ib; a.zb = (float*)zb; a.g = g2;
+    rc = launch_velocity_adj2d<float>(g2, k.radius, tp, a, false, as_stream(stream));
+  } else {
+    Taps<double> tp;
+    if ((rc = make_taps<double>(k, tp))) return rc;
+    VelAdjArgs<double> a{};
+    a.I = (const double*)I; a.z = (const double*)z; a.vbar = (const double*)vbar;
+    a.ib = (double*)ib; a.zb = (double*)zb; a.g = g2;
+    rc = launch_velocity_adj2d<double>(g2, k.radius, tp, a, false, as_stream(stream));
+  }
+  return check_rc(rc, "mr_velocity_adjoint");
+}
+
+int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps,
+                     void* traj_I, void* traj_z, void* traj_v, void* phi, int32_t* guard,
+                     void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (n_steps < 1) return fail(MR_EINVAL, "n_steps must be >= 1, got " + std::to_string(n_steps));
+  if (!(mu >= 0.0)) return fail(MR_EINVAL, "mu must be >= 0");
+  if (!traj_I || !traj_z || !traj_v) return fail(MR_EINVAL, "NULL trajectory pointer");
+  rc = MR_DISPATCH(dtype,
+                   shoot_forward<float>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
+                                        as_stream(stream)),
+                   shoot_forward<double>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
+                                         as_stream(stream)));
+  if (rc) return rc;
+  return check_cuda("mr_shoot_forward");
+}
+
+size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g) {
+  if (validate(dtype, g)) return 0;
+  size_t es = dtype == MR_F32 ? 4 : 8;
+  size_t S1 = (size_t)g.batch * (size_t)g.n[0] * (size_t)g.n[1];
+  return es * S1 * (4 + 2);
+}
+
+int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps, double lam,
+                     double rho, const void* traj_I, const void* traj_z, const void* traj_v,
+                     const void* J, void* zbar0, double* terms, int32_t* flags, void* workspace,
+                     void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (n_steps < 1) return fail(MR_EINVAL, "n_steps must be >= 1");
+  if (!(lam > 0.0)) return fail(MR_EINVAL, "lambda must be positive");
+  if (!(rho >= 0.0)) return fail(MR_EINVAL, "rho must be >= 0");
+  if (!traj_I || !traj_z || !traj_v || !J || !zbar0 || !terms || !flags || !workspace)
+    return fail(MR_EINVAL, "NULL pointer");
+  rc = MR_DISPATCH(dtype,
+                   shoot_adjoint<float>(g, k, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
+                                        zbar0, terms, flags, workspace, as_stream(stream)),
+                   shoot_adjoint<double>(g, k, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
+                                         zbar0, terms, flags, workspace, as_stream(stream)));
+  if (rc) return rc;
+  return check_cuda("mr_shoot_adjoint");
+}
+
+int mr_cost_terms(int dtype, mr_grid g, double lam, double rho, const void* I0, const void* z0,
+                  const void* v0, const void* IT, const void* J, double* terms, void* ibar_seed,
+                  void* stream) {
+  int rc = validate(dtype, g);
+  if (rc) return rc;
+  if (!I0 || !z0 || !v0 || !IT || !J || !terms) return fail(MR_EINVAL, "NULL pointer");
+  Grid2 g2 = grid2(g);
+  rc = MR_DISPATCH(dtype,
+                   launch_cost_terms2d<float>(g2, lam, rho, (const float*)I0, (const float*)z0,
+                                              (const float*)v0, (const float*)IT, (const float*)J,
+                                              terms, (float*)ibar_seed, as_stream(stream)),
+                   launch_cost_terms2d<double>(g2, lam, rho, (const double*)I0,
+                                               (const double*)z0, (const double*)v0,
+                                               (const double*)IT, (const double*)J, terms,
+                                               (double*)ibar_seed, as_stream(stream)));
+  return check_rc(rc, "mr_cost_terms");
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// mr_common.cuh -- shared device helpers for the sm_100a geodesic-shooting kernels.
+//
+// Semantics follow the reference package morphreg (/root/reference/pkg/src/morphreg);
+// every helper cites the line it restates.  See DESIGN.md for layouts and rooflines.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/morphreg_sm100.h"
+
+namespace mr {
+
+constexpr int kMaxR = MR_MAX_RADIUS;
+constexpr int kThreads = 256;
+
+// Gaussian taps passed BY VALUE as a kernel parameter: they live in the
+// constant bank, so with a compile-time radius every tap is an FFMA
+// constant-bank operand (no LDS/LDC per tap).
+//   w[t] : forward taps, t = 0..2R (symmetrised on the host)    kernel.py:24-31
+//   e[m] : cumulative sums W[m] = sum_{k<=m} w_k, m = 0..R, for the edge rows of
+//          the exact transpose (kernel.py:48-68)
+template <typename T>
+struct Taps {
+  T w[2 * kMaxR + 1];
+  T e[kMaxR + 1];
+};
+
+struct Grid2 {
+  int B, H, W;
+  long long N;  // H*W
+};
+
+// ---- finite differences (fields.py:144-158) ------------------------------------
+
+// np.gradient along one axis at index j of a length-n line, values at j-1, j, j+1
+// supplied by the caller (fm = f[j-1], f0 = f[j], fp = f[j+1]; unused ones ignored).
+template <typename T>
+__device__ __forceinline__ T grad1(T fm, T f0, T fp, int j, int n) {
+  if (j == 0) return fp - f0;
+  if (j == n - 1) return f0 - fm;
+  return (fp - fm) / T(2);
+}
+
+// Gather form of axis_diff_adjoint (fields.py:148-158) at index j:
+// gm = g[j-1], gp = g[j+1], g0 = g[0], gl = g[n-1] (caller passes what exists).
+// Term order follows the reference: edge updates first, then +0.5 g[j-1], -0.5 g[j+1].
+template <typename T>
+__device__ __forceinline__ T diff_adj1(T gm, T gp, T gfirst, T glast, int j, int n) {
+  T out = T(0);
+  if (j == 1) out += gfirst;
+  if (j == 0) out -= gfirst;
+  if (j == n - 1) out += glast;
+  if (j == n - 2) out -= glast;
+  if (j - 1 >= 1 && j - 1 <= n - 2) out += T(0.5) * gm;
+  if (j + 1 >= 1 && j + 1 <= n - 2) out -= T(0.5) * gp;
+  return out;
+}
+
+// ---- bilinear plan (fields.py:207-224) -------------------------------------------
+
+template <typename T>
+struct AxisPlan {
+  int i0;
+  T f;
+  bool inside;
+};
+
+// Foot coordinate pos - dt*vel on an axis of n samples, clamped to [0, n-1],
+// i0 = min(floor, n-2), strict inside mask (0 < y < n-1).
+// float: integer base + fractional displacement (SURVEY §7 hard part 2) so the
+// fraction keeps full fp32 precision far from the origin.
+// double: the reference's absolute-coordinate formula, rounding-identical.
+template <typename T>
+__device__ __forceinline__ AxisPlan<T> plan_axis(int pos, T vel, T dt, int n);
+
+template <>
+__device__ __forceinline__ AxisPlan<float> plan_axis<float>(int pos, float vel, float dt, int n) {
+  AxisPlan<float> p;
+  float d = -(dt * vel);
+  float fl = floorf(d);
+  float fr = d - fl;
+  // bound before the int conversion (huge values only occur after the guard fired)
+  fl = fminf(fmaxf(fl, -4.0f * n - 4.0f), 4.0f * n + 4.0f);
+  int ii = pos + (int)fl;
+  if (ii < 0 || (ii == 0 && fr == 0.0f)) {
+    p.i0 = 0; p.f = 0.0f; p.inside = false;
+  } else if (ii >= n - 1) {
+    p.i0 = n - 2; p.f = 1.0f; p.inside = false;
+  } else {
+    p.i0 = ii; p.f = fr; p.inside = true;
+  }
+  return p;
+}
+
+template <>
+__device__ __forceinline__ AxisPlan<double> plan_axis<double>(int pos, double vel, double dt, int n) {
+  AxisPlan<double> p;
+  double y = (double)pos + (-(dt * vel));
+  double yc = fmin(fmax(y, 0.0), (double)(n - 1));
+  if (!(yc == yc)) yc = 0.0;  // NaN: guard reports it; keep indices in range
+  int i0 = min((int)floor(yc), n - 2);
+  p.i0 = i0;
+  p.f = yc - (double)i0;
+  p.inside = (y > 0.0) && (y < (double)(n - 1));
+  return p;
+}
+
+// fields.py:235-240, same term order (bitwise-exact at nodes).
+template <typename T>
+__device__ __forceinline__ T bilerp(T a, T b, T c, T d, T fy, T fx) {
+  T wy = T(1) - fy, wx = T(1) - fx;
+  return wy * wx * a + fy * wx * b + wy * fx * c + fy * fx * d;
+}
+
+// ---- guard (integrator.py:113-118) -----------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ unsigned guard_bits(T x, unsigned nonfinite_bit) {
+  if (!isfinite(x)) return nonfinite_bit;
+  if (fabs(x) > T(1e6)) return nonfinite_bit << 1;
+  return 0u;
+}
+
+__device__ __forceinline__ void flush_flags(unsigned flags, int32_t* dst) {
+  unsigned all = __reduce_or_sync(0xffffffffu, flags);
+  if (all && (threadIdx.x & 31) == 0 && dst) atomicOr(reinterpret_cast<int*>(dst), (int)all);
+}
+
+}  // namespace mr
+
+#define MR_RADIUS_LIST(X)                                                       \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14)   \
+  X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26)      \
+  X(27) X(28) X(29) X(30) X(31) X(32)

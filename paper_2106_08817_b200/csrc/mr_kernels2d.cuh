@@ -1,0 +1,616 @@
+// mr_kernels2d.cuh -- 2D sm_100a kernels of the semi-Lagrangian shooting path.
+//
+// K1 k_velocity2d      v = -K*(z grad I)                 integrator.py:93-94
+// K2 k_sl_step2d       fused bilinear transport step       integrator.py:101-110,193-205
+// K3 k_sl_adjoint2d    transport adjoint (scatter + gathers) objective.py:118-147
+// K4 k_velocity_adj2d  -K^T, z-bar / i-bar stencil adjoint  objective.py:157-169
+// K5 k_cost_terms2d    SSD, <m0,K m0>, |z0|^2 (fp64 accum)  objective.py:64-88
+// plus k_smooth2d (smooth_arr / smooth_adjoint_arr, kernel.py:71-79).
+//
+// The separable Gaussian runs in a shared-memory tile engine (fir2d_tile): the
+// tile plus an R-pixel halo is staged in smem once, then a vertical and a
+// horizontal pass run with register blocking (RB outputs per thread, sliding
+// over RB+2R inputs) and the radius R as a template parameter so every tap is
+// an FFMA with a constant-bank weight.  Layout: SoA [B][c][H][W].
+#pragma once
+
+#include "mr_common.cuh"
+
+namespace mr {
+
+constexpr int kRB = 8;  // outputs per thread in each FIR pass
+
+// Output tile (OX x OY) of the FIR engine per precision.
+template <typename T> struct Tile2;
+template <> struct Tile2<float> { static constexpr int OX = 64, OY = 32; };
+template <> struct Tile2<double> { static constexpr int OX = 32, OY = 32; };
+
+template <typename T, int R, int C>
+struct FirSmem {
+  static constexpr int OX = Tile2<T>::OX, OY = Tile2<T>::OY;
+  static constexpr int RX = OX + 2 * R;  // region width (pitch)
+  static constexpr int RY = OY + 2 * R;
+  static constexpr int VP = RX + 1;      // pass-1 output pitch (odd: conflict-free rows)
+  static constexpr int OP = OX + 1;      // result pitch
+  static constexpr int region = C * RY * RX;
+  static constexpr int vt = C * OY * VP;
+  static constexpr size_t bytes = sizeof(T) * (size_t)(region + vt);
+  static_assert(C * OY * OP <= region, "result must fit in the region buffer");
+};
+
+// Separable FIR over one tile.  The region covering output rows
+// [y_org, y_org+OY) x cols [x_org, x_org+OX) plus an R halo is loaded through
+// `ld(gy, gx, out[C])`:
+//  - forward (TRANSPOSE=false): replicate borders, conv1d_replicate (kernel.py:36-45);
+//    clamped indices on load make the in-tile FIR exact.
+//  - transpose (TRANSPOSE=true): exact transpose conv1d_replicate_adjoint
+//    (kernel.py:48-68) = zero-padded correlation plus cumulative-weight edge
+//    rows/columns at index 0 and n-1.
+// Result: res[c*OY*OP + j*OP + i] (aliases the region buffer), valid after the
+// trailing __syncthreads.
+template <typename T, int R, int C, bool TRANSPOSE, class Loader>
+__device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_org, int y_org,
+                                               int H, int W, Loader ld) {
+  using S = FirSmem<T, R, C>;
+  constexpr int OX = S::OX, OY = S::OY, RX = S::RX, RY = S::RY, VP = S::VP, OP = S::OP;
+  T* rg = sm;
+  T* vt = sm + S::region;
+  const int tid = threadIdx.x;
+
+  // ---- stage the region (coalesced along x) ----
+  for (int p = tid; p < RY * RX; p += kThreads) {
+    int j = p / RX, i = p - j * RX;
+    int gy = y_org - R + j, gx = x_org - R + i;
+    T vals[C];
+    if (TRANSPOSE) {
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+        ld(gy, gx, vals);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) vals[c] = T(0);
+      }
+    } else {
+      gy = min(max(gy, 0), H - 1);
+      gx = min(max(gx, 0), W - 1);
+      ld(gy, gx, vals);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) rg[(c * RY + j) * RX + i] = vals[c];
+  }
+  __syncthreads();
+
+  // ---- pass 1: along axis 0 (rows), for every region column ----
+  constexpr int NB1 = OY / kRB;
+  for (int item = tid; item < C * RX * NB1; item += kThreads) {
+    int i = item % RX;
+    int rest = item / RX;
+    int jb = rest % NB1;
+    int c = rest / NB1;
+    const T* src = rg + (c * RY + jb * kRB) * RX + i;
+    T acc[kRB];
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+    for (int t = 0; t < kRB + 2 * R; ++t) {
+      T x = src[t * RX];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        const int tap = t - o;
+        if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+      }
+    }
+    if (TRANSPOSE) {
+      const int gy0 = y_org + jb * kRB;
+      if (gy0 <= 0 && gy0 + kRB > 0) {  // output row 0: sum_{d=0..R} W[R-d] g[d]
+        const int o = -gy0;
+        T s = T(0);
+#pragma unroll
+        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[(o + R + d) * RX], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+      if (gy0 <= H - 1 && gy0 + kRB > H - 1) {  // row n-1: sum_{d=-R..0} W[R+d] g[n-1+d]
+        const int o = H - 1 - gy0;
+        T s = T(0);
+#pragma unroll
+        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[(o + R + d) * RX], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+    }
+    T* dst = vt + (c * OY + jb * kRB) * VP + i;
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) dst[o * VP] = acc[o];
+  }
+  __syncthreads();
+
+  // ---- pass 2: along axis 1 (columns); lanes <-> rows (odd pitch) ----
+  constexpr int NB2 = OX / kRB;
+  T* res = rg;
+  for (int item = tid; item < C * OY * NB2; item += kThreads) {
+    int j = item % OY;
+    int rest = item / OY;
+    int ib = rest % NB2;
+    int c = rest / NB2;
+    const T* src = vt + (c * OY + j) * VP + ib * kRB;
+    T acc[kRB];
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+    for (int t = 0; t < kRB + 2 * R; ++t) {
+      T x = src[t];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        const int tap = t - o;
+        if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+      }
+    }
+    if (TRANSPOSE) {
+      const int gx0 = x_org + ib * kRB;
+      if (gx0 <= 0 && gx0 + kRB > 0) {
+        const int o = -gx0;
+        T s = T(0);
+#pragma unroll
+        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[o + R + d], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+      if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
+        const int o = W - 1 - gx0;
+        T s = T(0);
+#pragma unroll
+        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[o + R + d], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+    }
+    T* dst = res + (c * OY + j) * OP + ib * kRB;
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
+  }
+  __syncthreads();
+  return res;
+}
+
+// np.gradient of I at (y, x) along both axes (fields.py:144-145, 161-162).
+template <typename T>
+__device__ __forceinline__ void grad2(const T* __restrict__ I, int y, int x, int H, int W, T& g0,
+                                     T& g1) {
+  const long long row = (long long)y * W;
+  T c = I[row + x];
+  T up = (y > 0) ? I[row - W + x] : c;
+  T dn = (y < H - 1) ? I[row + W + x] : c;
+  T lf = (x > 0) ? I[row + x - 1] : c;
+  T rt = (x < W - 1) ? I[row + x + 1] : c;
+  g0 = grad1(up, c, dn, y, H);
+  g1 = grad1(lf, c, rt, x, W);
+}
+
+// ------------------------------------------------------------------------------
+// K1: v = -K*(z grad I) (+ guard on I, z, v)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct VelArgs {
+  const T* I;
+  const T* z;
+  T* v;
+  int32_t* guard;     // nullable, guard[b * guard_stride]
+  int guard_stride;
+  Grid2 g;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kThreads) k_velocity2d(VelArgs<T> a, Taps<T> tp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  using S = FirSmem<T, R, 2>;
+  const int H = a.g.H, W = a.g.W;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
+  const T* __restrict__ I = a.I + b * a.g.N;
+  const T* __restrict__ z = a.z + b * a.g.N;
+
+  auto ld = [&](int gy, int gx, T* out) {
+    T g0, g1;
+    grad2(I, gy, gx, H, W, g0, g1);
+    T zz = z[(long long)gy * W + gx];
+    out[0] = zz * g0;  // integrator.py:94  z[..., None] * grad_i
+    out[1] = zz * g1;
+  };
+  const T* res = fir2d_tile<T, R, 2, false>(sm, tp, x_org, y_org, H, W, ld);
+
+  unsigned flags = 0;
+  T* v0 = a.v + (long long)b * 2 * a.g.N;
+  T* v1 = v0 + a.g.N;
+  for (int p = threadIdx.x; p < S::OX * S::OY; p += kThreads) {
+    int j = p / S::OX, i = p - j * S::OX;
+    int gy = y_org + j, gx = x_org + i;
+    if (gy < H && gx < W) {
+      long long q = (long long)gy * W + gx;
+      T a0 = -res[j * S::OP + i];
+      T a1 = -res[(S::OY + j) * S::OP + i];
+      v0[q] = a0;
+      v1[q] = a1;
+      flags |= guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE);
+      flags |= guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
+      flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
+      flags |= guard_bits(a1, MR_GUARD_VELOCITY_NONFINITE);
+    }
+  }
+  if (a.guard) flush_flags(flags, a.guard + (long long)b * a.guard_stride);
+}
+
+// ------------------------------------------------------------------------------
+// smooth_arr / smooth_adjoint_arr on a scalar batch (kernel.py:71-79)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct SmoothArgs {
+  const T* a;
+  T* out;
+  Grid2 g;
+};
+
+template <typename T, int R, bool TRANSPOSE>
+__global__ void __launch_bounds__(kThreads) k_smooth2d(SmoothArgs<T> a, Taps<T> tp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  using S = FirSmem<T, R, 1>;
+  const int H = a.g.H, W = a.g.W;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
+  const T* __restrict__ src = a.a + b * a.g.N;
+  auto ld = [&](int gy, int gx, T* out) { out[0] = src[(long long)gy * W + gx]; };
+  const T* res = fir2d_tile<T, R, 1, TRANSPOSE>(sm, tp, x_org, y_org, H, W, ld);
+  T* dst = a.out + b * a.g.N;
+  for (int p = threadIdx.x; p < S::OX * S::OY; p += kThreads) {
+    int j = p / S::OX, i = p - j * S::OX;
+    int gy = y_org + j, gx = x_org + i;
+    if (gy < H && gx < W) dst[(long long)gy * W + gx] = res[j * S::OP + i];
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K2: one semi-Lagrangian step (integrator.py:101-110, 193-205)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct StepArgs {
+  const T* I;
+  const T* z;
+  const T* v;
+  T* In;
+  T* zn;
+  const T* phi_in;  // nullable
+  T* phi_out;
+  T dt, dtmu;
+  bool has_mu;
+  Grid2 g;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sl_step2d(StepArgs<T> a) {
+  const int H = a.g.H, W = a.g.W;
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * (kThreads / 32) + (threadIdx.x >> 5);
+  const int b = blockIdx.z;
+  if (x >= W || y >= H) return;
+  const long long N = a.g.N;
+  const long long q = (long long)y * W + x;
+  const T* __restrict__ I = a.I + b * N;
+  const T* __restrict__ z = a.z + b * N;
+  const T* __restrict__ v0 = a.v + b * 2 * N;
+  const T* __restrict__ v1 = v0 + N;
+  const T vy = v0[q], vx = v1[q];
+  const AxisPlan<T> py = plan_axis<T>(y, vy, a.dt, H);
+  const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
+  const long long c00 = (long long)py.i0 * W + px.i0;
+  const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
+  T bi = bilerp(I[c00], I[c10], I[c01], I[c11], py.f, px.f);
+  if (a.has_mu) bi = bi + a.dtmu * z[q];  // advect_image_sl_arr: + dt*mu*z
+  const T bz = bilerp(z[c00], z[c10], z[c01], z[c11], py.f, px.f);
+  // divergence_arr (fields.py:169-170)
+  const T up = (y > 0) ? v0[q - W] : vy;
+  const T dn = (y < H - 1) ? v0[q + W] : vy;
+  const T lf = (x > 0) ? v1[q - 1] : vx;
+  const T rt = (x < W - 1) ? v1[q + 1] : vx;
+  const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
+  a.In[b * N + q] = bi;
+  a.zn[b * N + q] = bz * (T(1) - a.dt * div);
+  if (a.phi_in) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const T* __restrict__ ph = a.phi_in + (b * 2 + c) * N;
+      a.phi_out[(b * 2 + c) * N + q] = bilerp(ph[c00], ph[c10], ph[c01], ph[c11], py.f, px.f);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_identity2d(T* phi, Grid2 g) {
+  long long n = (long long)g.B * g.N;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    long long b = p / g.N, q = p - b * g.N;
+    int y = (int)(q / g.W), x = (int)(q - (long long)y * g.W);
+    phi[(b * 2 + 0) * g.N + q] = T(y);
+    phi[(b * 2 + 1) * g.N + q] = T(x);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K3: adjoint of one SL step (objective.py:118-147, SL branches)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct AdjArgs {
+  const T* I;
+  const T* z;
+  const T* v;
+  const T* ibar;  // adjoint of I_{k+1}
+  const T* zbar;  // adjoint of z_{k+1}
+  T* ib;          // scatter target (zeroed)
+  T* zb;          // scatter target (zeroed)
+  T* vbar;        // [B][2][N] output
+  T dt, dtmu;
+  bool has_mu;
+  Grid2 g;
+};
+
+constexpr int kAdjTX = 32, kAdjTY = kThreads / 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
+  __shared__ T s_div[kAdjTY + 2][kAdjTX + 2];  // s = -dt * zbar * B(z), halo 1
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * kAdjTX, y0 = blockIdx.y * kAdjTY;
+  const T* __restrict__ I = a.I + b * N;
+  const T* __restrict__ z = a.z + b * N;
+  const T* __restrict__ v0 = a.v + b * 2 * N;
+  const T* __restrict__ v1 = v0 + N;
+  const T* __restrict__ ibar = a.ibar + b * N;
+  const T* __restrict__ zbar = a.zbar + b * N;
+  const T dt = a.dt;
+
+  // s on the tile + 1 halo (needed by the divergence adjoint, objective.py:145-147)
+  for (int p = threadIdx.x; p < (kAdjTY + 2) * (kAdjTX + 2); p += kThreads) {
+    int j = p / (kAdjTX + 2), i = p - j * (kAdjTX + 2);
+    int gy = y0 - 1 + j, gx = x0 - 1 + i;
+    T s = T(0);
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+      long long q = (long long)gy * W + gx;
+      AxisPlan<T> py = plan_axis<T>(gy, v0[q], dt, H);
+      AxisPlan<T> px = plan_axis<T>(gx, v1[q], dt, W);
+      long long c00 = (long long)py.i0 * W + px.i0;
+      T bz = bilerp(z[c00], z[c00 + W], z[c00 + 1], z[c00 + W + 1], py.f, px.f);
+      s = -dt * (zbar[q] * bz);
+    }
+    s_div[j][i] = s;
+  }
+  __syncthreads();
+
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x = x0 + tx, y = y0 + ty;
+  if (x >= W || y >= H) return;
+  const long long q = (long long)y * W + x;
+  const T vy = v0[q], vx = v1[q];
+  const AxisPlan<T> py = plan_axis<T>(y, vy, dt, H);
+  const AxisPlan<T> px = plan_axis<T>(x, vx, dt, W);
+  const long long c00 = (long long)py.i0 * W + px.i0;
+  const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
+  const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
+  const T ib_ = ibar[q];
+  const T zb_ = zbar[q];
+
+  // image update: ib = P^T ibar; vbar = -dt * dB(I)/dcoord * ibar (objective.py:128-132)
+  T* __restrict__ ibo = a.ib + b * N;
+  T* __restrict__ zbo = a.zb + b * N;
+  atomicAdd(ibo + c00, wy * wx * ib_);
+  atomicAdd(ibo + c10, fy * wx * ib_);
+  atomicAdd(ibo + c01, wy * fx * ib_);
+  atomicAdd(ibo + c11, fy * fx * ib_);
+  {
+    T ia = I[c00], ib2 = I[c10], ic = I[c01], id = I[c11];
+    T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
+    T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
+    T vb0 = -dt * ddy * ib_;
+    T vb1 = -dt * ddx * ib_;
+    // momentum update (objective.py:136-147)
+    const T up = (y > 0) ? v0[q - W] : vy;
+    const T dn = (y < H - 1) ? v0[q + W] : vy;
+    const T lf = (x > 0) ? v1[q - 1] : vx;
+    const T rt = (x < W - 1) ? v1[q + 1] : vx;
+    const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
+    const T scale = T(1) - dt * div;
+    const T wz = zb_ * scale;
+    if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);  // zb = dt*mu*ibar (:133)
+    atomicAdd(zbo + c00, wy * wx * wz);
+    atomicAdd(zbo + c10, fy * wx * wz);
+    atomicAdd(zbo + c01, wy * fx * wz);
+    atomicAdd(zbo + c11, fy * fx * wz);
+    T za = z[c00], zb2 = z[c10], zc = z[c01], zd = z[c11];
+    T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
+    T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
+    vb0 += -dt * dzy * wz;
+    vb1 += -dt * dzx * wz;
+    // divergence adjoint: vbar_c += D_c^T s (objective.py:145-147)
+    const int j = ty + 1, i = tx + 1;
+    const T sm_ = s_div[j - 1][i], sp_ = s_div[j + 1][i];
+    const T s_first_y = (y <= 1) ? s_div[j - y][i] : T(0);
+    const T s_last_y = (y >= H - 2) ? s_div[j + (H - 1 - y)][i] : T(0);
+    vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+    const T sl_ = s_div[j][i - 1], sr_ = s_div[j][i + 1];
+    const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
+    const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
+    vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    a.vbar[b * 2 * N + q] = vb0;
+    a.vbar[b * 2 * N + N + q] = vb1;
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K4: adjoint of v = -K*(z grad I) (objective.py:157-161); REG adds the
+// regulariser gradient at k = 0 (objective.py:165-169).
+// ------------------------------------------------------------------------------
+template <typename T>
+struct VelAdjArgs {
+  const T* I;
+  const T* z;
+  const T* vbar;   // [B][2][N]
+  T* ib;           // in/out: ib_acc -> ibar_k (unused when REG)
+  T* zb;           // in/out: zb_acc -> zbar_k
+  // REG only
+  const T* v0;     // forward v at k = 0
+  T* zout;         // dH/dz0
+  int32_t* flags;  // per pair non-finite flag
+  T lam, two_rho;
+  Grid2 g;
+};
+
+template <typename T, int R, bool REG>
+__global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Taps<T> tp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  using S = FirSmem<T, R, 2>;
+  constexpr int OX = S::OX, OY = S::OY, OP = S::OP;
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * (OX - 2) - 1, y_org = blockIdx.y * (OY - 2) - 1;
+  const T* __restrict__ I = a.I + b * N;
+  const T* __restrict__ z = a.z + b * N;
+  const T* __restrict__ vb0 = a.vbar + b * 2 * N;
+  const T* __restrict__ vb1 = vb0 + N;
+  const T lam = a.lam;
+
+  auto ld = [&](int gy, int gx, T* out) {
+    long long q = (long long)gy * W + gx;
+    out[0] = vb0[q];
+    out[1] = vb1[q];
+    if (REG) {  // feed vbar - lam*m0 so -K^T(.) also yields +lam K^T m0
+      T g0, g1;
+      grad2(I, gy, gx, H, W, g0, g1);
+      T zz = z[q];
+      out[0] = out[0] - lam * (zz * g0);
+      out[1] = out[1] - lam * (zz * g1);
+    }
+  };
+  const T* res = fir2d_tile<T, R, 2, true>(sm, tp, x_org, y_org, H, W, ld);
+
+  unsigned bad = 0;
+  for (int p = threadIdx.x; p < (OX - 2) * (OY - 2); p += kThreads) {
+    int jj = p / (OX - 2), ii = p - jj * (OX - 2);
+    int j = jj + 1, i = ii + 1;
+    int gy = y_org + j, gx = x_org + i;
+    if (gy >= H || gx >= W) continue;
+    long long q = (long long)gy * W + gx;
+    T g0, g1;
+    grad2(I, gy, gx, H, W, g0, g1);
+    const T m0 = -res[j * OP + i];
+    const T m1 = -res[(OY + j) * OP + i];
+    T zb_new = a.zb[b * N + q] + (m0 * g0 + m1 * g1);  // objective.py:159
+    if (REG) {
+      // + lam*(K m0 . grad I0 + 2 rho z0) with K m0 = -v0 (K^T m0 came through the FIR)
+      const T* __restrict__ w0 = a.v0 + b * 2 * N;
+      T km = -(w0[q] * g0 + w0[N + q] * g1);
+      zb_new = zb_new + lam * (km + a.two_rho * z[q]);
+      a.zout[b * N + q] = zb_new;
+      bad |= isfinite(zb_new) ? 0u : 1u;
+    } else {
+      a.zb[b * N + q] = zb_new;
+      // ib += G^T(mbar z) (objective.py:160-161), gather form on q_c = mbar_c * z
+      auto q0 = [&](int yy) { return -res[(yy - y_org) * OP + i] * z[(long long)yy * W + gx]; };
+      auto q1 = [&](int xx) { return -res[(OY + j) * OP + (xx - x_org)] * z[(long long)gy * W + xx]; };
+      T zc = z[q];
+      T qc0 = m0 * zc, qc1 = m1 * zc;
+      T gm = (gy > 0) ? q0(gy - 1) : T(0);
+      T gp = (gy < H - 1) ? q0(gy + 1) : T(0);
+      T gf = (gy == 0) ? qc0 : ((gy == 1) ? gm : T(0));
+      T gl = (gy == H - 1) ? qc0 : ((gy == H - 2) ? gp : T(0));
+      T t0 = diff_adj1(gm, gp, gf, gl, gy, H);
+      T hm = (gx > 0) ? q1(gx - 1) : T(0);
+      T hp = (gx < W - 1) ? q1(gx + 1) : T(0);
+      T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
+      T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
+      T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
+      a.ib[b * N + q] = a.ib[b * N + q] + (t0 + t1);
+    }
+  }
+  if (REG) {
+    unsigned all = __reduce_or_sync(0xffffffffu, bad);
+    if (all && (threadIdx.x & 31) == 0) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K5: cost terms (objective.py:64-88, fields.py:291-295, kernel.py:103-108)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct CostArgs {
+  const T* I0;
+  const T* z0;
+  const T* v0;
+  const T* IT;
+  const T* J;
+  T* seed;  // nullable: I_T - J
+  double* terms;  // [B][4] (zeroed): {total, data, v_norm, z_norm}
+  Grid2 g;
+};
+
+static __device__ __forceinline__ double block_sum(double x, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (l < (int)(blockDim.x >> 5)) ? red[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid on thread 0
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_cost_terms2d(CostArgs<T> a) {
+  __shared__ double red[kThreads / 32];
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.y;
+  const T* __restrict__ I0 = a.I0 + b * N;
+  const T* __restrict__ z0 = a.z0 + b * N;
+  const T* __restrict__ w0 = a.v0 + b * 2 * N;
+  const T* __restrict__ IT = a.IT + b * N;
+  const T* __restrict__ J = a.J + b * N;
+  double data = 0.0, vn = 0.0, zn = 0.0;
+  for (long long q = blockIdx.x * (long long)kThreads + threadIdx.x; q < N;
+       q += (long long)gridDim.x * kThreads) {
+    T diff = IT[q] - J[q];
+    if (a.seed) a.seed[b * N + q] = diff;
+    data += (double)diff * (double)diff;
+    int y = (int)(q / W), x = (int)(q - (long long)y * W);
+    T g0, g1;
+    grad2(I0, y, x, H, W, g0, g1);
+    T zz = z0[q];
+    vn += (double)(zz * g0) * (double)w0[q] + (double)(zz * g1) * (double)w0[N + q];
+    zn += (double)zz * (double)zz;
+  }
+  double s;
+  s = block_sum(data, red);
+  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 1], 0.5 * s);
+  s = block_sum(vn, red);
+  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 2], -s);
+  s = block_sum(zn, red);
+  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 3], s);
+}
+
+static __global__ void k_finalize_terms(double* terms, int B, double lam, double rho) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) {
+    double* t = terms + b * 4;
+    t[0] = t[1] + lam * (t[2] + rho * t[3]);  // objective.py:87
+  }
+}
+
+}  // namespace mr

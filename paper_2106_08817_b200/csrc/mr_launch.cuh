@@ -1,0 +1,23 @@
+// mr_launch.cuh -- host-side launchers (templated on precision) shared by the
+// translation units.  The FIR-engine launchers (radius dispatch 1..MR_MAX_RADIUS)
+// are defined in mr_fir_impl.cuh and explicitly instantiated per precision in
+// mr_fir_f32.cu / mr_fir_f64.cu so the heavy unrolled kernels compile in parallel.
+#pragma once
+
+#include "mr_kernels2d.cuh"
+
+namespace mr {
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? MR_OK : MR_ECUDA; }
+
+template <typename T>
+int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
+                      int32_t* guard, int guard_stride, cudaStream_t s);
+template <typename T>
+int launch_smooth2d(const Grid2& g, int R, const Taps<T>& tp, const T* a, T* out, bool transpose,
+                    cudaStream_t s);
+template <typename T>
+int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdjArgs<T>& args,
+                          bool reg, cudaStream_t s);
+
+}  // namespace mr

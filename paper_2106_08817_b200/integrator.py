@@ -1,0 +1,157 @@
+"""Geodesic shooting with the reference's signatures (integrator.py:48-219).
+
+``shoot(i0, z0, cfg)`` runs the whole T-step semi-Lagrangian loop on the device
+through one ``mr_shoot_forward`` call (2T+1 kernels), then checks the device
+guard once and raises ``IntegrationDiverged(step, what)`` with the reference's
+text (integrator.py:113-118).  Only ``Scheme.SEMI_LAGRANGIAN`` is accelerated
+in this build; the Eulerian / hybrid schemes are the next rows of the scope
+table and raise ``NotImplementedError``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+
+from . import engine
+from .errors import FieldError, IntegrationDiverged
+from .fields import GridGeometry, SampleGrid, ScalarField, VectorField
+from .kernel import GaussianKernel
+
+MAGNITUDE_GUARD = 1e6  # integrator.py:36
+
+__all__ = [
+    "MAGNITUDE_GUARD",
+    "IntegrationDiverged",
+    "Scheme",
+    "ShootingConfig",
+    "GeodesicState",
+    "GeodesicTrajectory",
+    "velocity_from_momentum",
+    "shoot",
+    "shoot_lddmm",
+    "path_energy",
+]
+
+
+class Scheme(str, Enum):
+    EULERIAN = "eulerian"
+    SEMI_LAGRANGIAN = "semi-lagrangian"
+    HYBRID = "hybrid"
+
+
+@dataclass(frozen=True)
+class ShootingConfig:
+    """integrator.py:54-69; ``dtype`` selects the device precision (float32 default)."""
+
+    scheme: Scheme
+    n_steps: int
+    mu: float
+    kernel: GaussianKernel
+    dtype: torch.dtype = field(default=torch.float32, compare=False)
+
+    def __post_init__(self) -> None:
+        if self.n_steps < 1:
+            raise FieldError(f"n_steps must be >= 1, got {self.n_steps}")
+        if self.mu < 0:
+            raise FieldError(f"mu must be >= 0, got {self.mu}")
+
+    @property
+    def dt(self) -> float:
+        return 1.0 / self.n_steps
+
+
+@dataclass(frozen=True)
+class GeodesicState:
+    t: float
+    image: ScalarField
+    momentum: ScalarField
+    velocity: VectorField
+
+
+@dataclass(frozen=True)
+class GeodesicTrajectory:
+    states: list
+    deformation: SampleGrid
+    device: engine.DeviceTrajectory | None = None
+
+    @property
+    def final_image(self) -> ScalarField:
+        return self.states[-1].image
+
+
+def _require_sl(cfg: ShootingConfig) -> None:
+    if cfg.scheme is not Scheme.SEMI_LAGRANGIAN:
+        raise NotImplementedError(
+            f"scheme {cfg.scheme.value!r} is not accelerated in this build "
+            "(semi-lagrangian only; see SURVEY.md §8(f))"
+        )
+
+
+def _to_device(f, dtype) -> torch.Tensor:
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return f.tensor.to(dev, dtype).contiguous()
+
+
+def velocity_from_momentum(z: ScalarField, image: ScalarField, kernel: GaussianKernel,
+                           dtype=torch.float32) -> VectorField:
+    """v = -K * (z grad I) (integrator.py:124-130)."""
+    if z.geometry != image.geometry:
+        raise FieldError("momentum/image geometry mismatch")
+    I = _to_device(image, dtype).unsqueeze(0)
+    zz = _to_device(z, dtype).unsqueeze(0)
+    v = engine.velocity(I, zz, kernel.weights)[0]
+    return VectorField(z.geometry, v, channel_first=True, _trusted=True)
+
+
+def _run(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig, mu: float) -> GeodesicTrajectory:
+    if i0.geometry != z0.geometry:
+        raise FieldError("image/momentum geometry mismatch")
+    _require_sl(cfg)
+    geom = i0.geometry
+    traj = engine.allocate_trajectory(1, geom.shape, cfg.n_steps, cfg.dtype, with_phi=True)
+    traj.I[0, 0].copy_(_to_device(i0, cfg.dtype))
+    traj.z[0, 0].copy_(_to_device(z0, cfg.dtype))
+    engine.shoot_forward(traj, mu, cfg.kernel.weights)
+    engine.raise_on_guard(traj)
+    dt = cfg.dt
+    states = []
+    for k in range(cfg.n_steps + 1):
+        states.append(
+            GeodesicState(
+                t=(k * dt if k < cfg.n_steps else 1.0),
+                image=ScalarField(geom, traj.I[k, 0], _trusted=True),
+                momentum=ScalarField(geom, traj.z[k, 0], _trusted=True),
+                velocity=VectorField(geom, traj.v[k, 0], channel_first=True, _trusted=True),
+            )
+        )
+    phi = SampleGrid(geom, traj.phi[0, 0], channel_first=True, _trusted=True)
+    return GeodesicTrajectory(states=states, deformation=phi, device=traj)
+
+
+def shoot(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig) -> GeodesicTrajectory:
+    """Integrate the geodesic system from (i0, z0) over unit time (integrator.py:163-219)."""
+    return _run(i0, z0, cfg, cfg.mu)
+
+
+def shoot_lddmm(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig) -> GeodesicTrajectory:
+    """Deformation-only shooting (integrator.py:222-277): the mu = 0 path of the
+    same kernels, so ``shoot`` with mu = 0 reproduces it bit for bit."""
+    return _run(i0, z0, cfg, 0.0)
+
+
+def path_energy(traj: GeodesicTrajectory, kernel: GaussianKernel, rho: float) -> list:
+    """Per-state ||v_t||_V^2 + rho ||z_t||^2 (integrator.py:280-289) = -<m_t, v_t> + rho|z_t|^2."""
+    if traj.device is None:
+        raise FieldError("path_energy needs a device trajectory from shoot()")
+    dev = traj.device
+    T = dev.n_steps
+    B = dev.batch
+    out = []
+    for k in range(T + 1):
+        terms = engine.cost_terms(dev.I[k], dev.z[k], dev.v[k], dev.I[k], dev.I[k], 1.0, rho)
+        t = terms.cpu().numpy()
+        out.append(float(t[0, 2] + rho * t[0, 3]) if B == 1 else [float(x) for x in t[:, 2] + rho * t[:, 3]])
+    return out

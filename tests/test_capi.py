@@ -1,0 +1,97 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every
+symbol include/morphreg_sm100.h declares; host logic needs no GPU."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO, load_golden
+
+HEADER = os.path.join(REPO, "include", "morphreg_sm100.h")
+LIB = os.path.join(REPO, "paper_2106_08817_b200", "libmorphreg_sm100.so")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mr_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_expected_entry_points():
+    from paper_2106_08817_b200 import _lib
+
+    assert declared_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(LIB):
+        pytest.fail(f"{LIB} not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    lib.mr_version.restype = ctypes.c_int
+    assert lib.mr_version() == 1
+
+
+def test_library_rejects_bad_arguments_without_gpu():
+    """Validation happens before any CUDA call, so it runs on the CPU host."""
+    from paper_2106_08817_b200 import _lib
+
+    lib = _lib.load_library(require_cuda=False)
+    g = _lib.make_grid(1, (1, 5))
+    rc = lib.mr_velocity(0, g, _lib.KernelHandle(np.ones(3) / 3).struct, None, None, None, None, None)
+    assert rc == 1
+    assert b"at least 2x2" in lib.mr_last_error()
+    g = _lib.make_grid(1, (8, 8))
+    k = _lib.MrKernel()
+    k.radius = 40
+    assert lib.mr_adjoint_workspace_bytes(0, g) == 8 * 8 * 6 * 4
+    assert lib.mr_adjoint_workspace_bytes(1, g) == 8 * 8 * 6 * 8
+    with pytest.raises(Exception):
+        _lib.KernelHandle(np.ones(81) / 81)  # radius 40 > MR_MAX_RADIUS
+
+
+def test_product_path_fails_loudly_without_cuda(monkeypatch):
+    import torch
+
+    from paper_2106_08817_b200 import _lib
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.load_library()
+
+
+def test_package_never_imports_the_oracle():
+    pkg = os.path.join(REPO, "paper_2106_08817_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(root, f)).read()
+                assert "oracle" not in src.replace("oracle/", ""), f
+
+
+def test_config1_generator_reproduces_golden_inputs():
+    from paper_2106_08817_b200.synthetic import make_config
+
+    g = load_golden("config1.npz")
+    c = make_config(1)
+    assert np.allclose(c.source[0], g["source"], rtol=0, atol=1e-15)
+    assert np.allclose(c.target[0], g["target"], rtol=0, atol=1e-15)
+    assert np.allclose(c.z0[0], g["z0"], rtol=0, atol=1e-17)
+
+
+def test_guard_bit_order_matches_reference_check_order():
+    from paper_2106_08817_b200 import _lib
+    from paper_2106_08817_b200.engine import guard_report
+
+    import torch
+
+    g = torch.zeros((2, 5), dtype=torch.int32)
+    assert guard_report(g) is None
+    g[1, 3] = (1 << 5) | (1 << 2)  # velocity magnitude + momentum non-finite
+    g[1, 4] = 1
+    assert guard_report(g) == (1, 3, "non-finite momentum")
+    assert [w for _, w in _lib.GUARD_BITS][0] == "non-finite image"
