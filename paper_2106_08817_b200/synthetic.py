@@ -12,6 +12,7 @@ these are seeded stand-ins with the configs' shapes, sizes and value ranges.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -257,29 +258,37 @@ def make_config(idx: int, seed: int = 0, batch: int | None = None, pairs=None,
     shp = tuple(shape) if shape is not None else spec["shape"]
     if pairs is None:
         pairs = list(range(batch if batch is not None else spec["batch"]))
-    srcs, tgts, zs = [], [], []
     manifest = {"config": idx, "seed": seed, "pairs": list(pairs), "shape": list(shp),
                 "ambiguities": "SURVEY.md Appendix C"}
-    for p in pairs:
+    if idx not in CONFIGS:
+        raise ValueError(f"unknown config {idx}")
+
+    def one(p):
         s = seed + p
         if idx == 1:
-            a, b, z = _config1(s, shp)
-        elif idx == 2:
-            a, b, z = _config2_pair(s, spec, shp)
-        elif idx in (3, 4):
+            return _config1(s, shp) + (None,)
+        if idx == 2:
+            return _config2_pair(s, spec, shp) + (None,)
+        if idx in (3, 4):
             scale = 1.0 if idx == 3 else 128.0 / 192.0
             if shape is not None:
                 scale *= shp[1] / spec["shape"][1]
-            lr = 14.0 * (scale if idx == 3 else 1.0) if idx == 3 else None
-            a, b, z, r = _brain_pair(s, shp, scale, lr, spec)
-            manifest.setdefault("lesion_radius", []).append(r)
-        elif idx == 5:
-            a, b, z = _stress_pair(s, shp, spec)
-        else:
-            raise ValueError(f"unknown config {idx}")
-        srcs.append(a)
-        tgts.append(b)
-        zs.append(z)
+            lr = 14.0 * scale if idx == 3 else None
+            return _brain_pair(s, shp, scale, lr, spec)
+        return _stress_pair(s, shp, spec) + (None,)
+
+    # pairs are independent and seeded per pair: generate them concurrently
+    # (scipy's correlate1d releases the GIL); results do not depend on order
+    from concurrent.futures import ThreadPoolExecutor
+
+    workers = max(1, min(len(pairs), os.cpu_count() or 1, 16))
+    with ThreadPoolExecutor(workers) as ex:
+        out = list(ex.map(one, pairs))
+    srcs = [o[0] for o in out]
+    tgts = [o[1] for o in out]
+    zs = [o[2] for o in out]
+    if idx in (3, 4):
+        manifest["lesion_radius"] = [o[3] for o in out]
     return ConfigData(
         name=spec["name"], source=np.stack(srcs), target=np.stack(tgts), z0=np.stack(zs),
         n_steps=spec["n_steps"], sigma=spec["sigma"], radius=spec["radius"], mu=spec["mu"],
