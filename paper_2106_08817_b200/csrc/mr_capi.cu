@@ -97,8 +97,8 @@ static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, co
 template <typename T>
 static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I, const T* z,
                                const T* v, const T* ibar, const T* zbar, T* ib, T* zb, T* vbar,
-                               cudaStream_t s) {
-  AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, g};
+                               cudaStream_t s, double reg_lam = 0.0) {
+  AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, (T)reg_lam, g};
   dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjTY - 1) / kAdjTY, g.B);
   k_sl_adjoint2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
@@ -186,7 +186,7 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
   for (int step = T_ - 1; step >= 0; --step) {
     if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
     rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
-                                cur + S1, acc, acc + S1, vbar, s);
+                                cur + S1, acc, acc + S1, vbar, s, step == 0 ? lam : 0.0);
     if (rc) return check_rc(rc, "sl_adjoint");
     VelAdjArgs<T> a{};
     a.I = I + step * S1;

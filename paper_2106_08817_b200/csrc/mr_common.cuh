@@ -127,6 +127,27 @@ __device__ __forceinline__ void flush_flags(unsigned flags, int32_t* dst) {
   if (all && (threadIdx.x & 31) == 0 && dst) atomicOr(reinterpret_cast<int*>(dst), (int)all);
 }
 
+// ---- cp.async (LDGSTS) staging: many loads in flight, no register round trip ----
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem),
+               "n"((int)sizeof(T)));
+}
+
+// zero-fills the destination when !valid (src-size 0; gmem must still be a valid address)
+template <typename T>
+__device__ __forceinline__ void cp_async_elem_zfill(T* smem, const T* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? (int)sizeof(T) : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+               "n"((int)sizeof(T)), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 }  // namespace mr
 
 #define MR_RADIUS_LIST(X)                                                       \

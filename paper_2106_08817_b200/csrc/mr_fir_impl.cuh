@@ -12,10 +12,11 @@ inline dim3 fir_grid(int W, int H, int B, int tx, int ty) {
 template <typename T, int R>
 int velocity_r(const Grid2& g, const Taps<T>& tp, const VelArgs<T>& a, cudaStream_t s) {
   using S = FirSmem<T, R, 2>;
+  constexpr size_t bytes = VelSmem<T, R>::bytes;
   static const cudaError_t attr = cudaFuncSetAttribute(
-      k_velocity2d<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+      k_velocity2d<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (attr != cudaSuccess) return MR_ECUDA;
-  k_velocity2d<T, R><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, S::bytes, s>>>(a, tp);
+  k_velocity2d<T, R><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, bytes, s>>>(a, tp);
   return cuda_status(cudaGetLastError());
 }
 
@@ -32,11 +33,12 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
 template <typename T, int R, bool REG>
 int veladj_r(const Grid2& g, const Taps<T>& tp, const VelAdjArgs<T>& a, cudaStream_t s) {
   using S = FirSmem<T, R, 2>;
+  constexpr size_t bytes = VelAdjSmem<T, R>::bytes;
   static const cudaError_t attr = cudaFuncSetAttribute(
-      k_velocity_adj2d<T, R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+      k_velocity_adj2d<T, R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (attr != cudaSuccess) return MR_ECUDA;
   k_velocity_adj2d<T, R, REG>
-      <<<fir_grid(g.W, g.H, g.B, S::OX - 2, S::OY - 2), kThreads, S::bytes, s>>>(a, tp);
+      <<<fir_grid(g.W, g.H, g.B, S::OX - 2, S::OY - 2), kThreads, bytes, s>>>(a, tp);
   return cuda_status(cudaGetLastError());
 }
 

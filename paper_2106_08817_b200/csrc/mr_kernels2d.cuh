@@ -38,47 +38,29 @@ struct FirSmem {
   static_assert(C * OY * OP <= region, "result must fit in the region buffer");
 };
 
-// Separable FIR over one tile.  The region covering output rows
-// [y_org, y_org+OY) x cols [x_org, x_org+OX) plus an R halo is loaded through
-// `ld(gy, gx, out[C])`:
-//  - forward (TRANSPOSE=false): replicate borders, conv1d_replicate (kernel.py:36-45);
-//    clamped indices on load make the in-tile FIR exact.
+// Separable FIR passes over one staged tile.  rg holds the region
+// [c][RY][RX] covering output rows [y_org, y_org+OY) x cols [x_org, x_org+OX)
+// plus an R halo:
+//  - forward (TRANSPOSE=false): replicate borders (conv1d_replicate,
+//    kernel.py:36-45) -- the region holds clamped-index samples, so the in-tile
+//    FIR is exact.
 //  - transpose (TRANSPOSE=true): exact transpose conv1d_replicate_adjoint
 //    (kernel.py:48-68) = zero-padded correlation plus cumulative-weight edge
-//    rows/columns at index 0 and n-1.
-// Result: res[c*OY*OP + j*OP + i] (aliases the region buffer), valid after the
-// trailing __syncthreads.
-template <typename T, int R, int C, bool TRANSPOSE, class Loader>
-__device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_org, int y_org,
-                                               int H, int W, Loader ld) {
+//    rows/columns at index 0 and n-1; the region holds
+//    zeros outside the image.
+// Pass 1 runs along axis 0 for every region column (register blocking kRB
+// outputs per thread, sliding over kRB+2R inputs), pass 2 along axis 1 with
+// lanes mapped to rows (odd pitch: conflict-free).  The result
+// res[c*OY*OP + j*OP + i] aliases the FIRST C*OY*OP elements of rg; the rest
+// of rg is free from the start of pass 2 (see `mid`, called between passes,
+// e.g. to issue cp.async prefetches of epilogue operands into rg's tail).
+// Caller must __syncthreads() before reading res.
+template <typename T, int R, int C, bool TRANSPOSE, class Mid>
+__device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp, int x_org,
+                                                 int y_org, int H, int W, Mid mid) {
   using S = FirSmem<T, R, C>;
   constexpr int OX = S::OX, OY = S::OY, RX = S::RX, RY = S::RY, VP = S::VP, OP = S::OP;
-  T* rg = sm;
-  T* vt = sm + S::region;
   const int tid = threadIdx.x;
-
-  // ---- stage the region (coalesced along x) ----
-  for (int p = tid; p < RY * RX; p += kThreads) {
-    int j = p / RX, i = p - j * RX;
-    int gy = y_org - R + j, gx = x_org - R + i;
-    T vals[C];
-    if (TRANSPOSE) {
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-        ld(gy, gx, vals);
-      } else {
-#pragma unroll
-        for (int c = 0; c < C; ++c) vals[c] = T(0);
-      }
-    } else {
-      gy = min(max(gy, 0), H - 1);
-      gx = min(max(gx, 0), W - 1);
-      ld(gy, gx, vals);
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) rg[(c * RY + j) * RX + i] = vals[c];
-  }
-  __syncthreads();
-
   // ---- pass 1: along axis 0 (rows), for every region column ----
   constexpr int NB1 = OY / kRB;
   for (int item = tid; item < C * RX * NB1; item += kThreads) {
@@ -123,6 +105,7 @@ __device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_o
     for (int o = 0; o < kRB; ++o) dst[o * VP] = acc[o];
   }
   __syncthreads();
+  mid();
 
   // ---- pass 2: along axis 1 (columns); lanes <-> rows (odd pitch) ----
   constexpr int NB2 = OX / kRB;
@@ -168,6 +151,44 @@ __device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_o
 #pragma unroll
     for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
   }
+  return res;
+}
+
+struct NoMid {
+  __device__ void operator()() const {}
+};
+
+// Generic tile: staging through `ld(gy, gx, out[C])` (clamped / zero-padded as
+// above), then the passes.  Used by the smoothing entry points and the k = 0
+// regulariser variant; the hot kernels stage with cp.async instead.
+template <typename T, int R, int C, bool TRANSPOSE, class Loader>
+__device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_org, int y_org,
+                                               int H, int W, Loader ld) {
+  using S = FirSmem<T, R, C>;
+  constexpr int RX = S::RX, RY = S::RY;
+  T* rg = sm;
+  T* vt = sm + S::region;
+  for (int p = threadIdx.x; p < RY * RX; p += kThreads) {
+    int j = p / RX, i = p - j * RX;
+    int gy = y_org - R + j, gx = x_org - R + i;
+    T vals[C];
+    if (TRANSPOSE) {
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+        ld(gy, gx, vals);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) vals[c] = T(0);
+      }
+    } else {
+      gy = min(max(gy, 0), H - 1);
+      gx = min(max(gx, 0), W - 1);
+      ld(gy, gx, vals);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) rg[(c * RY + j) * RX + i] = vals[c];
+  }
+  __syncthreads();
+  const T* res = fir2d_passes<T, R, C, TRANSPOSE>(rg, vt, tp, x_org, y_org, H, W, NoMid{});
   __syncthreads();
   return res;
 }
@@ -199,30 +220,93 @@ struct VelArgs {
   Grid2 g;
 };
 
+// smem of K1: region rg[2][RY][RX] | union{ I stage [(RY+2)][(RX+2)], pass-1 output }
+template <typename T, int R>
+struct VelSmem {
+  using S = FirSmem<T, R, 2>;
+  static constexpr int IP = S::RX + 2;  // I stage pitch
+  static constexpr int istage = (S::RY + 2) * IP;
+  static constexpr int aux = istage > S::vt ? istage : S::vt;
+  static constexpr size_t bytes = sizeof(T) * (size_t)(S::region + aux);
+};
+
 template <typename T, int R>
 __global__ void __launch_bounds__(kThreads) k_velocity2d(VelArgs<T> a, Taps<T> tp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
   using S = FirSmem<T, R, 2>;
+  using V = VelSmem<T, R>;
+  constexpr int RX = S::RX, RY = S::RY, IP = V::IP;
+  T* rg = reinterpret_cast<T*>(smem_raw);
+  T* m0 = rg;
+  T* m1 = rg + RY * RX;
+  T* ist = rg + S::region;  // I stage; later the pass-1 output
   const int H = a.g.H, W = a.g.W;
   const int b = blockIdx.z;
   const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
   const T* __restrict__ I = a.I + b * a.g.N;
   const T* __restrict__ z = a.z + b * a.g.N;
+  const int tid = threadIdx.x;
 
-  auto ld = [&](int gy, int gx, T* out) {
-    T g0, g1;
-    grad2(I, gy, gx, H, W, g0, g1);
-    T zz = z[(long long)gy * W + gx];
-    out[0] = zz * g0;  // integrator.py:94  z[..., None] * grad_i
-    out[1] = zz * g1;
-  };
-  const T* res = fir2d_tile<T, R, 2, false>(sm, tp, x_org, y_org, H, W, ld);
+  // ---- stage I (region + 1) and z (region) with clamped indices, all in flight ----
+  for (int p = tid; p < (RY + 2) * IP; p += kThreads) {
+    int j = p / IP, i = p - j * IP;
+    int gy = min(max(y_org - R - 1 + j, 0), H - 1);
+    int gx = min(max(x_org - R - 1 + i, 0), W - 1);
+    cp_async_elem(ist + p, I + (long long)gy * W + gx);
+  }
+  for (int p = tid; p < RY * RX; p += kThreads) {
+    int j = p / RX, i = p - j * RX;
+    int gy = min(max(y_org - R + j, 0), H - 1);
+    int gx = min(max(x_org - R + i, 0), W - 1);
+    cp_async_elem(m1 + p, z + (long long)gy * W + gx);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
 
+  // ---- m = z grad I at in-image region samples (integrator.py:94); guard I, z ----
   unsigned flags = 0;
+  bool clamped_tile = false;
+  for (int p = tid; p < RY * RX; p += kThreads) {
+    int j = p / RX, i = p - j * RX;
+    int uy = y_org - R + j, ux = x_org - R + i;
+    if (uy < 0 || uy >= H || ux < 0 || ux >= W) {
+      clamped_tile = true;
+      continue;
+    }
+    const T* c = ist + (j + 1) * IP + (i + 1);
+    T f0 = c[0];
+    T g0 = grad1(c[-IP], f0, c[IP], uy, H);
+    T g1 = grad1(c[-1], f0, c[1], ux, W);
+    T zz = m1[p];
+    m0[p] = zz * g0;
+    m1[p] = zz * g1;
+    if (j >= R && j < R + S::OY && i >= R && i < R + S::OX) {
+      flags |= guard_bits(f0, MR_GUARD_IMAGE_NONFINITE);
+      flags |= guard_bits(zz, MR_GUARD_MOMENTUM_NONFINITE);
+    }
+  }
+  // border tiles: replicate the border samples into the clamped halo
+  if (__syncthreads_or(clamped_tile)) {
+    for (int p = tid; p < RY * RX; p += kThreads) {
+      int j = p / RX, i = p - j * RX;
+      int uy = y_org - R + j, ux = x_org - R + i;
+      int gy = min(max(uy, 0), H - 1), gx = min(max(ux, 0), W - 1);
+      if (gy != uy || gx != ux) {
+        int q = (gy - (y_org - R)) * RX + (gx - (x_org - R));
+        m0[p] = m0[q];
+        m1[p] = m1[q];
+      }
+    }
+    __syncthreads();
+  }
+
+  const T* res = fir2d_passes<T, R, 2, false>(rg, ist, tp, x_org, y_org, H, W, NoMid{});
+  __syncthreads();
+
   T* v0 = a.v + (long long)b * 2 * a.g.N;
   T* v1 = v0 + a.g.N;
-  for (int p = threadIdx.x; p < S::OX * S::OY; p += kThreads) {
+  for (int p = tid; p < S::OX * S::OY; p += kThreads) {
     int j = p / S::OX, i = p - j * S::OX;
     int gy = y_org + j, gx = x_org + i;
     if (gy < H && gx < W) {
@@ -231,8 +315,6 @@ __global__ void __launch_bounds__(kThreads) k_velocity2d(VelArgs<T> a, Taps<T> t
       T a1 = -res[(S::OY + j) * S::OP + i];
       v0[q] = a0;
       v1[q] = a1;
-      flags |= guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE);
-      flags |= guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
       flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
       flags |= guard_bits(a1, MR_GUARD_VELOCITY_NONFINITE);
     }
@@ -351,6 +433,7 @@ struct AdjArgs {
   T* vbar;        // [B][2][N] output
   T dt, dtmu;
   bool has_mu;
+  T reg_lam;  // k = 0 only: vbar -= reg_lam * z grad I (regulariser fold)
   Grid2 g;
 };
 
@@ -442,6 +525,13 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
     const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
     const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
     vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    if (a.reg_lam != T(0)) {
+      T g0, g1;
+      grad2(I, y, x, H, W, g0, g1);
+      const T zz = z[q];
+      vb0 = vb0 - a.reg_lam * (zz * g0);
+      vb1 = vb1 - a.reg_lam * (zz * g1);
+    }
     a.vbar[b * 2 * N + q] = vb0;
     a.vbar[b * 2 * N + N + q] = vb1;
   }
@@ -466,12 +556,26 @@ struct VelAdjArgs {
   Grid2 g;
 };
 
+// smem of K4: region rg (padded so that, once pass 1 is done, its tail holds the
+// epilogue operands [5][OY][OX] next to the result) | pass-1 output vt.
+template <typename T, int R>
+struct VelAdjSmem {
+  using S = FirSmem<T, R, 2>;
+  static constexpr int OXY = S::OX * S::OY;
+  static constexpr int res = 2 * S::OY * S::OP;
+  static constexpr int rg = S::region > res + 5 * OXY ? S::region : res + 5 * OXY;
+  static constexpr size_t bytes = sizeof(T) * (size_t)(rg + S::vt);
+};
+
 template <typename T, int R, bool REG>
 __global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Taps<T> tp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
   using S = FirSmem<T, R, 2>;
-  constexpr int OX = S::OX, OY = S::OY, OP = S::OP;
+  using V = VelAdjSmem<T, R>;
+  constexpr int OX = S::OX, OY = S::OY, OP = S::OP, RX = S::RX, RY = S::RY, OXY = V::OXY;
+  T* rg = reinterpret_cast<T*>(smem_raw);
+  T* vt = rg + V::rg;
+  T* tail = rg + V::res;  // [5][OY][OX]: I, z, ib|v0_0, zb, -|v0_1
   const int H = a.g.H, W = a.g.W;
   const long long N = a.g.N;
   const int b = blockIdx.z;
@@ -480,59 +584,87 @@ __global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Ta
   const T* __restrict__ z = a.z + b * N;
   const T* __restrict__ vb0 = a.vbar + b * 2 * N;
   const T* __restrict__ vb1 = vb0 + N;
-  const T lam = a.lam;
+  const int tid = threadIdx.x;
 
-  auto ld = [&](int gy, int gx, T* out) {
-    long long q = (long long)gy * W + gx;
-    out[0] = vb0[q];
-    out[1] = vb1[q];
-    if (REG) {  // feed vbar - lam*m0 so -K^T(.) also yields +lam K^T m0
-      T g0, g1;
-      grad2(I, gy, gx, H, W, g0, g1);
-      T zz = z[q];
-      out[0] = out[0] - lam * (zz * g0);
-      out[1] = out[1] - lam * (zz * g1);
+  // ---- stage vbar (zero outside the image), all loads in flight ----
+  // (at k = 0 the transport adjoint already folded -lam*m0 into vbar, so
+  //  -K^T(vbar - lam m0) also yields the +lam K^T m0 regulariser term, A.17)
+  for (int p = tid; p < RY * RX; p += kThreads) {
+    int j = p / RX, i = p - j * RX;
+    int gy = y_org - R + j, gx = x_org - R + i;
+    bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+    long long q = in ? (long long)gy * W + gx : 0;
+    cp_async_elem_zfill(rg + p, vb0 + q, in);
+    cp_async_elem_zfill(rg + RY * RX + p, vb1 + q, in);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+
+  // prefetch the epilogue operands into rg's tail while pass 2 runs
+  auto prefetch = [&]() {
+    const T* src2 = REG ? a.v0 + b * 2 * N : a.ib + b * N;
+    const T* src4 = REG ? a.v0 + b * 2 * N + N : nullptr;
+    for (int p = tid; p < OXY; p += kThreads) {
+      int j = p / OX, i = p - j * OX;
+      int gy = y_org + j, gx = x_org + i;
+      bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+      long long q = in ? (long long)gy * W + gx : 0;
+      cp_async_elem_zfill(tail + p, I + q, in);
+      cp_async_elem_zfill(tail + OXY + p, z + q, in);
+      cp_async_elem_zfill(tail + 2 * OXY + p, src2 + q, in);
+      cp_async_elem_zfill(tail + 3 * OXY + p, a.zb + b * N + q, in);
+      if (REG) cp_async_elem_zfill(tail + 4 * OXY + p, src4 + q, in);
     }
+    cp_async_commit();
   };
-  const T* res = fir2d_tile<T, R, 2, true>(sm, tp, x_org, y_org, H, W, ld);
+  const T* res = fir2d_passes<T, R, 2, true>(rg, vt, tp, x_org, y_org, H, W, prefetch);
+  cp_async_wait_all();
+  __syncthreads();
 
+  const T* tI = tail;
+  const T* tz = tail + OXY;
+  const T* t2 = tail + 2 * OXY;
+  const T* tzb = tail + 3 * OXY;
+  const T* t4 = tail + 4 * OXY;
   unsigned bad = 0;
-  for (int p = threadIdx.x; p < (OX - 2) * (OY - 2); p += kThreads) {
+  for (int p = tid; p < (OX - 2) * (OY - 2); p += kThreads) {
     int jj = p / (OX - 2), ii = p - jj * (OX - 2);
     int j = jj + 1, i = ii + 1;
     int gy = y_org + j, gx = x_org + i;
     if (gy >= H || gx >= W) continue;
     long long q = (long long)gy * W + gx;
-    T g0, g1;
-    grad2(I, gy, gx, H, W, g0, g1);
+    const int e = j * OX + i;
+    const T c = tI[e];
+    const T g0 = grad1(tI[e - OX], c, tI[e + OX], gy, H);
+    const T g1 = grad1(tI[e - 1], c, tI[e + 1], gx, W);
     const T m0 = -res[j * OP + i];
     const T m1 = -res[(OY + j) * OP + i];
-    T zb_new = a.zb[b * N + q] + (m0 * g0 + m1 * g1);  // objective.py:159
+    T zb_new = tzb[e] + (m0 * g0 + m1 * g1);  // objective.py:159
     if (REG) {
-      // + lam*(K m0 . grad I0 + 2 rho z0) with K m0 = -v0 (K^T m0 came through the FIR)
-      const T* __restrict__ w0 = a.v0 + b * 2 * N;
-      T km = -(w0[q] * g0 + w0[N + q] * g1);
-      zb_new = zb_new + lam * (km + a.two_rho * z[q]);
+      // + lam*(K m0 . grad I0 + 2 rho z0) with K m0 = -v0 (objective.py:165-169)
+      T km = -(t2[e] * g0 + t4[e] * g1);
+      zb_new = zb_new + a.lam * (km + a.two_rho * tz[e]);
       a.zout[b * N + q] = zb_new;
       bad |= isfinite(zb_new) ? 0u : 1u;
     } else {
       a.zb[b * N + q] = zb_new;
       // ib += G^T(mbar z) (objective.py:160-161), gather form on q_c = mbar_c * z
-      auto q0 = [&](int yy) { return -res[(yy - y_org) * OP + i] * z[(long long)yy * W + gx]; };
-      auto q1 = [&](int xx) { return -res[(OY + j) * OP + (xx - x_org)] * z[(long long)gy * W + xx]; };
-      T zc = z[q];
-      T qc0 = m0 * zc, qc1 = m1 * zc;
-      T gm = (gy > 0) ? q0(gy - 1) : T(0);
-      T gp = (gy < H - 1) ? q0(gy + 1) : T(0);
-      T gf = (gy == 0) ? qc0 : ((gy == 1) ? gm : T(0));
-      T gl = (gy == H - 1) ? qc0 : ((gy == H - 2) ? gp : T(0));
-      T t0 = diff_adj1(gm, gp, gf, gl, gy, H);
-      T hm = (gx > 0) ? q1(gx - 1) : T(0);
-      T hp = (gx < W - 1) ? q1(gx + 1) : T(0);
-      T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
-      T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
-      T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
-      a.ib[b * N + q] = a.ib[b * N + q] + (t0 + t1);
+      auto q0 = [&](int jr) { return -res[jr * OP + i] * tz[jr * OX + i]; };
+      auto q1 = [&](int ic) { return -res[(OY + j) * OP + ic] * tz[j * OX + ic]; };
+      const T zc = tz[e];
+      const T qc0 = m0 * zc, qc1 = m1 * zc;
+      const T gm = (gy > 0) ? q0(j - 1) : T(0);
+      const T gp = (gy < H - 1) ? q0(j + 1) : T(0);
+      const T gf = (gy == 0) ? qc0 : ((gy == 1) ? gm : T(0));
+      const T gl = (gy == H - 1) ? qc0 : ((gy == H - 2) ? gp : T(0));
+      const T t0 = diff_adj1(gm, gp, gf, gl, gy, H);
+      const T hm = (gx > 0) ? q1(i - 1) : T(0);
+      const T hp = (gx < W - 1) ? q1(i + 1) : T(0);
+      const T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
+      const T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
+      const T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
+      a.ib[b * N + q] = t2[e] + (t0 + t1);
     }
   }
   if (REG) {
