@@ -33,6 +33,8 @@ static int check_rc(int rc, const char* where) {
   if (rc == MR_OK) return MR_OK;
   if (rc < 0) {
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = g_last_cuda;
+    g_last_cuda = cudaSuccess;
     return fail(rc, std::string(where) + ": " + cudaGetErrorString(e));
   }
   return fail(rc, std::string(where) + ": invalid argument");

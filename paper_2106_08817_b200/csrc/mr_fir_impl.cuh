@@ -2,6 +2,7 @@
 #pragma once
 
 #include "mr_launch.cuh"
+#include "mr_tma.h"
 
 namespace mr {
 
@@ -10,13 +11,18 @@ inline dim3 fir_grid(int W, int H, int B, int tx, int ty) {
 }
 
 template <typename T, int R>
-int velocity_r(const Grid2& g, const Taps<T>& tp, const VelArgs<T>& a, cudaStream_t s) {
+int velocity_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
   using S = FirSmem<T, R, 2>;
-  constexpr size_t bytes = VelSmem<T, R>::bytes;
+  using V = VelSmem<T, R>;
+  constexpr size_t bytes = V::bytes;
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_velocity2d<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (attr != cudaSuccess) return MR_ECUDA;
-  k_velocity2d<T, R><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, bytes, s>>>(a, tp);
+  if (attr != cudaSuccess) return cuda_status(attr);
+  CUtensorMap mI, mZ;
+  a.use_tma = make_map3<T>(&mI, a.I, g.W, g.H, g.B, V::PXI, S::RY + 2) &&
+              make_map3<T>(&mZ, a.z, g.W, g.H, g.B, S::PX, S::RY);
+  k_velocity2d<T, R>
+      <<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, bytes, s>>>(a, tp, mI, mZ);
   return cuda_status(cudaGetLastError());
 }
 
@@ -25,27 +31,36 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
   using S = FirSmem<T, R, 1>;
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_smooth2d<T, R, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
-  if (attr != cudaSuccess) return MR_ECUDA;
+  if (attr != cudaSuccess) return cuda_status(attr);
   k_smooth2d<T, R, TR><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, S::bytes, s>>>(a, tp);
   return cuda_status(cudaGetLastError());
 }
 
 template <typename T, int R, bool REG>
-int veladj_r(const Grid2& g, const Taps<T>& tp, const VelAdjArgs<T>& a, cudaStream_t s) {
+int veladj_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
   using S = FirSmem<T, R, 2>;
+  using V = VelAdjSmem<T, R>;
   constexpr size_t bytes = VelAdjSmem<T, R>::bytes;
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_velocity_adj2d<T, R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (attr != cudaSuccess) return MR_ECUDA;
+  if (attr != cudaSuccess) return cuda_status(attr);
+  VelAdjMaps m;
+  const long long B2 = 2LL * g.B;
+  a.use_tma = make_map3<T>(&m.vbar, a.vbar, g.W, g.H, B2, S::PX, S::RY) &&
+              make_map3<T>(&m.I, a.I, g.W, g.H, g.B, V::OXP, S::OY) &&
+              make_map3<T>(&m.z, a.z, g.W, g.H, g.B, V::OXP, S::OY) &&
+              (REG ? make_map3<T>(&m.op2, a.v0, g.W, g.H, B2, V::OXP, S::OY)
+                   : make_map3<T>(&m.op2, a.ib, g.W, g.H, g.B, V::OXP, S::OY)) &&
+              make_map3<T>(&m.zb, a.zb, g.W, g.H, g.B, V::OXP, S::OY);
   k_velocity_adj2d<T, R, REG>
-      <<<fir_grid(g.W, g.H, g.B, S::OX - 2, S::OY - 2), kThreads, bytes, s>>>(a, tp);
+      <<<fir_grid(g.W, g.H, g.B, S::OX - 2, S::OY - 2), kThreads, bytes, s>>>(a, tp, m);
   return cuda_status(cudaGetLastError());
 }
 
 template <typename T>
 int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
                       int32_t* guard, int guard_stride, cudaStream_t s) {
-  VelArgs<T> a{I, z, v, guard, guard_stride, g};
+  VelArgs<T> a{I, z, v, guard, guard_stride, 0, g};
   switch (R) {
 #define MR_CASE(RR) \
   case RR: return velocity_r<T, RR>(g, tp, a, s);

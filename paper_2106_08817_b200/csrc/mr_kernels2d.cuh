@@ -19,6 +19,12 @@
 namespace mr {
 
 constexpr int kRB = 8;  // outputs per thread in each FIR pass
+constexpr int kNW = kThreads / 32;
+
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// shift of a box starting at column x0 relative to the aligned column below it
+__device__ __forceinline__ int align_shift(int x0, int A) { return ((x0 % A) + A) % A; }
 
 // Output tile (OX x OY) of the FIR engine per precision.
 template <typename T> struct Tile2;
@@ -28,18 +34,24 @@ template <> struct Tile2<double> { static constexpr int OX = 32, OY = 32; };
 template <typename T, int R, int C>
 struct FirSmem {
   static constexpr int OX = Tile2<T>::OX, OY = Tile2<T>::OY;
-  static constexpr int RX = OX + 2 * R;  // region width (pitch)
+  static constexpr int RX = OX + 2 * R;  // region width
   static constexpr int RY = OY + 2 * R;
+  // TMA boxes must start at a 16-byte aligned column: a box starts at the
+  // aligned column at or below the wanted one and the smem view is shifted by
+  // the remainder (0 .. A-1 elements), so the pitch leaves room for it.
+  static constexpr int A = 16 / (int)sizeof(T);
+  static constexpr int PX = round_up(RX + A - 1, A);  // region pitch = TMA box width
   static constexpr int VP = RX + 1;      // pass-1 output pitch (odd: conflict-free rows)
   static constexpr int OP = OX + 1;      // result pitch
-  static constexpr int region = C * RY * RX;
-  static constexpr int vt = C * OY * VP;
+  static constexpr int CS = round_up(RY * PX, 32);  // component stride (128-B aligned TMA dst)
+  static constexpr int region = round_up(C * CS + A, 32);
+  static constexpr int vt = round_up(C * OY * VP, 32);
   static constexpr size_t bytes = sizeof(T) * (size_t)(region + vt);
   static_assert(C * OY * OP <= region, "result must fit in the region buffer");
 };
 
 // Separable FIR passes over one staged tile.  rg holds the region
-// [c][RY][RX] covering output rows [y_org, y_org+OY) x cols [x_org, x_org+OX)
+// [c][RY][PX] covering output rows [y_org, y_org+OY) x cols [x_org, x_org+OX)
 // plus an R halo:
 //  - forward (TRANSPOSE=false): replicate borders (conv1d_replicate,
 //    kernel.py:36-45) -- the region holds clamped-index samples, so the in-tile
@@ -52,29 +64,30 @@ struct FirSmem {
 // outputs per thread, sliding over kRB+2R inputs), pass 2 along axis 1 with
 // lanes mapped to rows (odd pitch: conflict-free).  The result
 // res[c*OY*OP + j*OP + i] aliases the FIRST C*OY*OP elements of rg; the rest
-// of rg is free from the start of pass 2 (see `mid`, called between passes,
-// e.g. to issue cp.async prefetches of epilogue operands into rg's tail).
+// of rg is free from the start of pass 2 (`mid` runs between the passes, e.g.
+// to issue prefetches of epilogue operands into rg's tail).
 // Caller must __syncthreads() before reading res.
 template <typename T, int R, int C, bool TRANSPOSE, class Mid>
 __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp, int x_org,
                                                  int y_org, int H, int W, Mid mid) {
   using S = FirSmem<T, R, C>;
-  constexpr int OX = S::OX, OY = S::OY, RX = S::RX, RY = S::RY, VP = S::VP, OP = S::OP;
+  constexpr int OX = S::OX, OY = S::OY, RX = S::RX, PX = S::PX, VP = S::VP, OP = S::OP,
+                CS = S::CS;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   // ---- pass 1: along axis 0 (rows), for every region column ----
   constexpr int NB1 = OY / kRB;
-  for (int item = tid; item < C * RX * NB1; item += kThreads) {
-    int i = item % RX;
-    int rest = item / RX;
-    int jb = rest % NB1;
-    int c = rest / NB1;
-    const T* src = rg + (c * RY + jb * kRB) * RX + i;
+  for (int cb = warp; cb < C * NB1; cb += kNW)
+  for (int i = lane; i < RX; i += 32) {
+    const int jb = cb % NB1;
+    const int c = cb / NB1;
+    const T* src = rg + c * CS + jb * kRB * PX + i;
     T acc[kRB];
 #pragma unroll
     for (int o = 0; o < kRB; ++o) acc[o] = T(0);
 #pragma unroll
     for (int t = 0; t < kRB + 2 * R; ++t) {
-      T x = src[t * RX];
+      T x = src[t * PX];
 #pragma unroll
       for (int o = 0; o < kRB; ++o) {
         const int tap = t - o;
@@ -87,7 +100,7 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
         const int o = -gy0;
         T s = T(0);
 #pragma unroll
-        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[(o + R + d) * RX], s);
+        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[(o + R + d) * PX], s);
 #pragma unroll
         for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
       }
@@ -95,7 +108,7 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
         const int o = H - 1 - gy0;
         T s = T(0);
 #pragma unroll
-        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[(o + R + d) * RX], s);
+        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[(o + R + d) * PX], s);
 #pragma unroll
         for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
       }
@@ -110,11 +123,11 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
   // ---- pass 2: along axis 1 (columns); lanes <-> rows (odd pitch) ----
   constexpr int NB2 = OX / kRB;
   T* res = rg;
-  for (int item = tid; item < C * OY * NB2; item += kThreads) {
-    int j = item % OY;
-    int rest = item / OY;
-    int ib = rest % NB2;
-    int c = rest / NB2;
+  static_assert(OY == 32, "pass 2 maps lanes to the 32 rows of a tile");
+  for (int cb = warp; cb < C * NB2; cb += kNW) {
+    const int j = lane;
+    const int ib = cb % NB2;
+    const int c = cb / NB2;
     const T* src = vt + (c * OY + j) * VP + ib * kRB;
     T acc[kRB];
 #pragma unroll
@@ -159,34 +172,35 @@ struct NoMid {
 };
 
 // Generic tile: staging through `ld(gy, gx, out[C])` (clamped / zero-padded as
-// above), then the passes.  Used by the smoothing entry points and the k = 0
-// regulariser variant; the hot kernels stage with cp.async instead.
+// above), then the passes.  Used by the smoothing entry points; the hot
+// kernels stage with TMA (or cp.async) instead.
 template <typename T, int R, int C, bool TRANSPOSE, class Loader>
 __device__ __forceinline__ const T* fir2d_tile(T* sm, const Taps<T>& tp, int x_org, int y_org,
                                                int H, int W, Loader ld) {
   using S = FirSmem<T, R, C>;
-  constexpr int RX = S::RX, RY = S::RY;
+  constexpr int RX = S::RX, RY = S::RY, PX = S::PX, CS = S::CS;
   T* rg = sm;
   T* vt = sm + S::region;
-  for (int p = threadIdx.x; p < RY * RX; p += kThreads) {
-    int j = p / RX, i = p - j * RX;
-    int gy = y_org - R + j, gx = x_org - R + i;
-    T vals[C];
-    if (TRANSPOSE) {
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-        ld(gy, gx, vals);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < RY; j += kNW)
+    for (int i = lane; i < RX; i += 32) {
+      int gy = y_org - R + j, gx = x_org - R + i;
+      T vals[C];
+      if (TRANSPOSE) {
+        if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+          ld(gy, gx, vals);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) vals[c] = T(0);
+        }
       } else {
-#pragma unroll
-        for (int c = 0; c < C; ++c) vals[c] = T(0);
+        gy = min(max(gy, 0), H - 1);
+        gx = min(max(gx, 0), W - 1);
+        ld(gy, gx, vals);
       }
-    } else {
-      gy = min(max(gy, 0), H - 1);
-      gx = min(max(gx, 0), W - 1);
-      ld(gy, gx, vals);
-    }
 #pragma unroll
-    for (int c = 0; c < C; ++c) rg[(c * RY + j) * RX + i] = vals[c];
-  }
+      for (int c = 0; c < C; ++c) rg[c * CS + j * PX + i] = vals[c];
+    }
   __syncthreads();
   const T* res = fir2d_passes<T, R, C, TRANSPOSE>(rg, vt, tp, x_org, y_org, H, W, NoMid{});
   __syncthreads();
@@ -217,102 +231,136 @@ struct VelArgs {
   T* v;
   int32_t* guard;     // nullable, guard[b * guard_stride]
   int guard_stride;
+  int use_tma;        // tensor maps valid (else cp.async staging)
   Grid2 g;
 };
 
-// smem of K1: region rg[2][RY][RX] | union{ I stage [(RY+2)][(RX+2)], pass-1 output }
+// smem of K1: mbarrier | region m[2][RY][PX] (z staged into m[1]) |
+//             union{ I stage [(RY+2)][PXI], pass-1 output }
 template <typename T, int R>
 struct VelSmem {
   using S = FirSmem<T, R, 2>;
-  static constexpr int IP = S::RX + 2;  // I stage pitch
-  static constexpr int istage = (S::RY + 2) * IP;
+  static constexpr int PXI = round_up(S::RX + 2 + S::A - 1, S::A);  // I stage pitch / box width
+  static constexpr int istage = round_up((S::RY + 2) * PXI + S::A, 32);
   static constexpr int aux = istage > S::vt ? istage : S::vt;
-  static constexpr size_t bytes = sizeof(T) * (size_t)(S::region + aux);
+  static constexpr size_t head = 128;  // mbarriers
+  static constexpr size_t bytes = head + sizeof(T) * (size_t)(S::region + aux);
 };
 
 template <typename T, int R>
-__global__ void __launch_bounds__(kThreads) k_velocity2d(VelArgs<T> a, Taps<T> tp) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kThreads)
+    k_velocity2d(VelArgs<T> a, Taps<T> tp, const __grid_constant__ CUtensorMap mapI,
+                 const __grid_constant__ CUtensorMap mapZ) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using S = FirSmem<T, R, 2>;
   using V = VelSmem<T, R>;
-  constexpr int RX = S::RX, RY = S::RY, IP = V::IP;
-  T* rg = reinterpret_cast<T*>(smem_raw);
-  T* m0 = rg;
-  T* m1 = rg + RY * RX;
-  T* ist = rg + S::region;  // I stage; later the pass-1 output
+  constexpr int RX = S::RX, RY = S::RY, PX = S::PX, PXI = V::PXI;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  T* rg0 = reinterpret_cast<T*>(smem_raw + V::head);
+  T* ist0 = rg0 + S::region;  // I stage; later the pass-1 output
   const int H = a.g.H, W = a.g.W;
   const int b = blockIdx.z;
   const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
+  const int offZ = align_shift(x_org - R, S::A), offI = align_shift(x_org - R - 1, S::A);
+  T* rg = rg0 + offZ;  // region element (j, i) at rg[j*PX + i]
+  T* m0 = rg;
+  T* m1 = rg + S::CS;
+  T* ist = ist0 + offI;  // I stage element (j, i) at ist[j*PXI + i]
   const T* __restrict__ I = a.I + b * a.g.N;
   const T* __restrict__ z = a.z + b * a.g.N;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
 
-  // ---- stage I (region + 1) and z (region) with clamped indices, all in flight ----
-  for (int p = tid; p < (RY + 2) * IP; p += kThreads) {
-    int j = p / IP, i = p - j * IP;
-    int gy = min(max(y_org - R - 1 + j, 0), H - 1);
-    int gx = min(max(x_org - R - 1 + i, 0), W - 1);
-    cp_async_elem(ist + p, I + (long long)gy * W + gx);
+  // ---- stage I (region + 1) and z (region) ----
+  if (a.use_tma) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_barrier_init();
+      mbar_expect_tx(bar, (unsigned)(sizeof(T) * (PXI * (RY + 2) + PX * RY)));
+      tma_load_3d(ist0, &mapI, x_org - R - 1 - offI, y_org - R - 1, b, bar);
+      tma_load_3d(rg0 + S::CS, &mapZ, x_org - R - offZ, y_org - R, b, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+  } else {
+    for (int j = warp; j < RY + 2; j += kNW) {
+      const T* row = I + (long long)min(max(y_org - R - 1 + j, 0), H - 1) * W;
+      for (int i = lane; i < RX + 2; i += 32)
+        cp_async_elem(ist + j * PXI + i, row + min(max(x_org - R - 1 + i, 0), W - 1));
+    }
+    for (int j = warp; j < RY; j += kNW) {
+      const T* row = z + (long long)min(max(y_org - R + j, 0), H - 1) * W;
+      for (int i = lane; i < RX; i += 32)
+        cp_async_elem(m1 + j * PX + i, row + min(max(x_org - R + i, 0), W - 1));
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
   }
-  for (int p = tid; p < RY * RX; p += kThreads) {
-    int j = p / RX, i = p - j * RX;
-    int gy = min(max(y_org - R + j, 0), H - 1);
-    int gx = min(max(x_org - R + i, 0), W - 1);
-    cp_async_elem(m1 + p, z + (long long)gy * W + gx);
-  }
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncthreads();
 
   // ---- m = z grad I at in-image region samples (integrator.py:94); guard I, z ----
   unsigned flags = 0;
-  bool clamped_tile = false;
-  for (int p = tid; p < RY * RX; p += kThreads) {
-    int j = p / RX, i = p - j * RX;
-    int uy = y_org - R + j, ux = x_org - R + i;
-    if (uy < 0 || uy >= H || ux < 0 || ux >= W) {
-      clamped_tile = true;
-      continue;
-    }
-    const T* c = ist + (j + 1) * IP + (i + 1);
-    T f0 = c[0];
-    T g0 = grad1(c[-IP], f0, c[IP], uy, H);
-    T g1 = grad1(c[-1], f0, c[1], ux, W);
-    T zz = m1[p];
-    m0[p] = zz * g0;
-    m1[p] = zz * g1;
-    if (j >= R && j < R + S::OY && i >= R && i < R + S::OX) {
-      flags |= guard_bits(f0, MR_GUARD_IMAGE_NONFINITE);
-      flags |= guard_bits(zz, MR_GUARD_MOMENTUM_NONFINITE);
+  const int i_lo = max(0, R - x_org), i_hi = min(RX, W - x_org + R);  // in-image columns
+  const int j_lo = max(0, R - y_org), j_hi = min(RY, H - y_org + R);  // in-image rows
+  // interior tile: every in-image sample has both neighbours on both axes
+  const bool interior = (y_org - R >= 1) && (y_org - R + RY <= H - 1) && (x_org - R >= 1) &&
+                        (x_org - R + RX <= W - 1);
+  for (int j = j_lo + warp; j < j_hi; j += kNW) {
+    const int uy = y_org - R + j;
+    const bool own_row = j >= R && j < R + S::OY;
+    const T* crow = ist + (j + 1) * PXI + 1;
+    for (int i = i_lo + lane; i < i_hi; i += 32) {
+      const T* c = crow + i;
+      const T f0 = c[0];
+      T g0, g1;
+      if (interior) {
+        g0 = (c[PXI] - c[-PXI]) / T(2);
+        g1 = (c[1] - c[-1]) / T(2);
+      } else {
+        const int ux = x_org - R + i;
+        g0 = grad1(c[-PXI], f0, c[PXI], uy, H);
+        g1 = grad1(c[-1], f0, c[1], ux, W);
+      }
+      const int p = j * PX + i;
+      const T zz = m1[p];
+      m0[p] = zz * g0;
+      m1[p] = zz * g1;
+      if (own_row && i >= R && i < R + S::OX) {
+        flags |= guard_bits(f0, MR_GUARD_IMAGE_NONFINITE);
+        flags |= guard_bits(zz, MR_GUARD_MOMENTUM_NONFINITE);
+      }
     }
   }
+  __syncthreads();
   // border tiles: replicate the border samples into the clamped halo
-  if (__syncthreads_or(clamped_tile)) {
-    for (int p = tid; p < RY * RX; p += kThreads) {
-      int j = p / RX, i = p - j * RX;
-      int uy = y_org - R + j, ux = x_org - R + i;
-      int gy = min(max(uy, 0), H - 1), gx = min(max(ux, 0), W - 1);
-      if (gy != uy || gx != ux) {
-        int q = (gy - (y_org - R)) * RX + (gx - (x_org - R));
-        m0[p] = m0[q];
-        m1[p] = m1[q];
+  if (i_lo > 0 || j_lo > 0 || i_hi < RX || j_hi < RY) {
+    for (int j = warp; j < RY; j += kNW) {
+      const int jr = min(max(j, j_lo), j_hi - 1);
+      for (int i = lane; i < RX; i += 32) {
+        const int ir = min(max(i, i_lo), i_hi - 1);
+        if (jr != j || ir != i) {
+          m0[j * PX + i] = m0[jr * PX + ir];
+          m1[j * PX + i] = m1[jr * PX + ir];
+        }
       }
     }
     __syncthreads();
   }
 
-  const T* res = fir2d_passes<T, R, 2, false>(rg, ist, tp, x_org, y_org, H, W, NoMid{});
+  const T* res = fir2d_passes<T, R, 2, false>(rg, ist0, tp, x_org, y_org, H, W, NoMid{});
   __syncthreads();
 
   T* v0 = a.v + (long long)b * 2 * a.g.N;
   T* v1 = v0 + a.g.N;
-  for (int p = tid; p < S::OX * S::OY; p += kThreads) {
-    int j = p / S::OX, i = p - j * S::OX;
-    int gy = y_org + j, gx = x_org + i;
-    if (gy < H && gx < W) {
-      long long q = (long long)gy * W + gx;
-      T a0 = -res[j * S::OP + i];
-      T a1 = -res[(S::OY + j) * S::OP + i];
+  for (int j = warp; j < S::OY; j += kNW) {
+    const int gy = y_org + j;
+    if (gy >= H) break;
+    for (int i = lane; i < S::OX; i += 32) {
+      const int gx = x_org + i;
+      if (gx >= W) break;
+      const long long q = (long long)gy * W + gx;
+      const T a0 = -res[j * S::OP + i];
+      const T a1 = -res[(S::OY + j) * S::OP + i];
       v0[q] = a0;
       v1[q] = a1;
       flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
@@ -334,7 +382,7 @@ struct SmoothArgs {
 
 template <typename T, int R, bool TRANSPOSE>
 __global__ void __launch_bounds__(kThreads) k_smooth2d(SmoothArgs<T> a, Taps<T> tp) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   using S = FirSmem<T, R, 1>;
   const int H = a.g.H, W = a.g.W;
@@ -553,73 +601,129 @@ struct VelAdjArgs {
   T* zout;         // dH/dz0
   int32_t* flags;  // per pair non-finite flag
   T lam, two_rho;
+  int use_tma;
   Grid2 g;
 };
 
-// smem of K4: region rg (padded so that, once pass 1 is done, its tail holds the
-// epilogue operands [5][OY][OX] next to the result) | pass-1 output vt.
+// Tensor maps of K4: vbar (dims W,H,2B), then the epilogue operands
+// I, z, ib|v0 (W,H,B | W,H,2B), zb, v0 (REG, second component).
+struct VelAdjMaps {
+  CUtensorMap vbar, I, z, op2, zb;
+};
+
+// smem of K4: mbarriers | region rg (padded so that, once pass 1 is done, its
+// tail holds the epilogue operands [5][OY][OX] next to the result) | vt.
 template <typename T, int R>
 struct VelAdjSmem {
   using S = FirSmem<T, R, 2>;
-  static constexpr int OXY = S::OX * S::OY;
-  static constexpr int res = 2 * S::OY * S::OP;
+  static constexpr int OXP = S::OX + S::A;  // epilogue box width (room for the shift)
+  static constexpr int OXY = round_up(OXP * S::OY, 32);  // operand stride (128-B aligned)
+  static constexpr int res = round_up(2 * S::OY * S::OP + S::A, 32);
   static constexpr int rg = S::region > res + 5 * OXY ? S::region : res + 5 * OXY;
-  static constexpr size_t bytes = sizeof(T) * (size_t)(rg + S::vt);
+  static constexpr size_t head = 128;
+  static constexpr size_t bytes = head + sizeof(T) * (size_t)(rg + S::vt);
 };
 
 template <typename T, int R, bool REG>
-__global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Taps<T> tp) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kThreads)
+    k_velocity_adj2d(VelAdjArgs<T> a, Taps<T> tp, const __grid_constant__ VelAdjMaps maps) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   using S = FirSmem<T, R, 2>;
   using V = VelAdjSmem<T, R>;
-  constexpr int OX = S::OX, OY = S::OY, OP = S::OP, RX = S::RX, RY = S::RY, OXY = V::OXY;
-  T* rg = reinterpret_cast<T*>(smem_raw);
-  T* vt = rg + V::rg;
-  T* tail = rg + V::res;  // [5][OY][OX]: I, z, ib|v0_0, zb, -|v0_1
+  constexpr int OX = S::OX, OY = S::OY, OP = S::OP, RX = S::RX, RY = S::RY, PX = S::PX,
+                OXY = V::OXY, OXP = V::OXP;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  T* rg0 = reinterpret_cast<T*>(smem_raw + V::head);
+  T* vt = rg0 + V::rg;
+  T* tail0 = rg0 + V::res;  // [5][OY][OXP]: I, z, ib|v0_0, zb, -|v0_1
   const int H = a.g.H, W = a.g.W;
   const long long N = a.g.N;
   const int b = blockIdx.z;
   const int x_org = blockIdx.x * (OX - 2) - 1, y_org = blockIdx.y * (OY - 2) - 1;
+  const int offV = align_shift(x_org - R, S::A), offE = align_shift(x_org, S::A);
+  T* rg = rg0 + offV;      // region element (j, i) at rg[j*PX + i]
+  T* tail = tail0 + offE;  // operand k element (j, i) at tail[k*OXY + j*OXP + i]
   const T* __restrict__ I = a.I + b * N;
   const T* __restrict__ z = a.z + b * N;
   const T* __restrict__ vb0 = a.vbar + b * 2 * N;
   const T* __restrict__ vb1 = vb0 + N;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
 
-  // ---- stage vbar (zero outside the image), all loads in flight ----
+  // ---- stage vbar, zero outside the image ----
   // (at k = 0 the transport adjoint already folded -lam*m0 into vbar, so
   //  -K^T(vbar - lam m0) also yields the +lam K^T m0 regulariser term, A.17)
-  for (int p = tid; p < RY * RX; p += kThreads) {
-    int j = p / RX, i = p - j * RX;
-    int gy = y_org - R + j, gx = x_org - R + i;
-    bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-    long long q = in ? (long long)gy * W + gx : 0;
-    cp_async_elem_zfill(rg + p, vb0 + q, in);
-    cp_async_elem_zfill(rg + RY * RX + p, vb1 + q, in);
+  if (a.use_tma) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      fence_barrier_init();
+      mbar_expect_tx(bar, (unsigned)(sizeof(T) * 2 * PX * RY));
+      tma_load_3d(rg0, &maps.vbar, x_org - R - offV, y_org - R, 2 * b, bar);
+      tma_load_3d(rg0 + S::CS, &maps.vbar, x_org - R - offV, y_org - R, 2 * b + 1, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+  } else {
+    for (int j = warp; j < RY; j += kNW) {
+      const int gy = y_org - R + j;
+      const bool rin = gy >= 0 && gy < H;
+      const long long rq = rin ? (long long)gy * W : 0;
+      for (int i = lane; i < RX; i += 32) {
+        const int gx = x_org - R + i;
+        const bool in = rin && gx >= 0 && gx < W;
+        const long long q = in ? rq + gx : 0;
+        cp_async_elem_zfill(rg + j * PX + i, vb0 + q, in);
+        cp_async_elem_zfill(rg + S::CS + j * PX + i, vb1 + q, in);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
   }
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncthreads();
 
   // prefetch the epilogue operands into rg's tail while pass 2 runs
   auto prefetch = [&]() {
+    if (a.use_tma) {
+      if (tid == 0) {
+        // WAR across proxies: pass 1 read this smem through the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(bar + 1, (unsigned)(sizeof(T) * OXY * (REG ? 5 : 4)));
+        const int xa = x_org - offE;
+        tma_load_3d(tail0, &maps.I, xa, y_org, b, bar + 1);
+        tma_load_3d(tail0 + OXY, &maps.z, xa, y_org, b, bar + 1);
+        tma_load_3d(tail0 + 2 * OXY, &maps.op2, xa, y_org, REG ? 2 * b : b, bar + 1);
+        tma_load_3d(tail0 + 3 * OXY, &maps.zb, xa, y_org, b, bar + 1);
+        if (REG) tma_load_3d(tail0 + 4 * OXY, &maps.op2, xa, y_org, 2 * b + 1, bar + 1);
+      }
+      return;
+    }
     const T* src2 = REG ? a.v0 + b * 2 * N : a.ib + b * N;
     const T* src4 = REG ? a.v0 + b * 2 * N + N : nullptr;
-    for (int p = tid; p < OXY; p += kThreads) {
-      int j = p / OX, i = p - j * OX;
-      int gy = y_org + j, gx = x_org + i;
-      bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-      long long q = in ? (long long)gy * W + gx : 0;
-      cp_async_elem_zfill(tail + p, I + q, in);
-      cp_async_elem_zfill(tail + OXY + p, z + q, in);
-      cp_async_elem_zfill(tail + 2 * OXY + p, src2 + q, in);
-      cp_async_elem_zfill(tail + 3 * OXY + p, a.zb + b * N + q, in);
-      if (REG) cp_async_elem_zfill(tail + 4 * OXY + p, src4 + q, in);
+    for (int j = warp; j < OY; j += kNW) {
+      const int gy = y_org + j;
+      const bool rin = gy >= 0 && gy < H;
+      const long long rq = rin ? (long long)gy * W : 0;
+      for (int i = lane; i < OX; i += 32) {
+        const int gx = x_org + i;
+        const bool in = rin && gx >= 0 && gx < W;
+        const long long q = in ? rq + gx : 0;
+        const int p = j * OXP + i;
+        cp_async_elem_zfill(tail + p, I + q, in);
+        cp_async_elem_zfill(tail + OXY + p, z + q, in);
+        cp_async_elem_zfill(tail + 2 * OXY + p, src2 + q, in);
+        cp_async_elem_zfill(tail + 3 * OXY + p, a.zb + b * N + q, in);
+        if (REG) cp_async_elem_zfill(tail + 4 * OXY + p, src4 + q, in);
+      }
     }
     cp_async_commit();
   };
   const T* res = fir2d_passes<T, R, 2, true>(rg, vt, tp, x_org, y_org, H, W, prefetch);
-  cp_async_wait_all();
+  if (a.use_tma) {
+    mbar_wait(bar + 1, 0);
+  } else {
+    cp_async_wait_all();
+  }
   __syncthreads();
 
   const T* tI = tail;
@@ -628,15 +732,14 @@ __global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Ta
   const T* tzb = tail + 3 * OXY;
   const T* t4 = tail + 4 * OXY;
   unsigned bad = 0;
-  for (int p = tid; p < (OX - 2) * (OY - 2); p += kThreads) {
-    int jj = p / (OX - 2), ii = p - jj * (OX - 2);
-    int j = jj + 1, i = ii + 1;
-    int gy = y_org + j, gx = x_org + i;
+  for (int j = 1 + warp; j < OY - 1; j += kNW)
+  for (int i = 1 + lane; i < OX - 1; i += 32) {
+    const int gy = y_org + j, gx = x_org + i;
     if (gy >= H || gx >= W) continue;
     long long q = (long long)gy * W + gx;
-    const int e = j * OX + i;
+    const int e = j * OXP + i;
     const T c = tI[e];
-    const T g0 = grad1(tI[e - OX], c, tI[e + OX], gy, H);
+    const T g0 = grad1(tI[e - OXP], c, tI[e + OXP], gy, H);
     const T g1 = grad1(tI[e - 1], c, tI[e + 1], gx, W);
     const T m0 = -res[j * OP + i];
     const T m1 = -res[(OY + j) * OP + i];
@@ -650,8 +753,8 @@ __global__ void __launch_bounds__(kThreads) k_velocity_adj2d(VelAdjArgs<T> a, Ta
     } else {
       a.zb[b * N + q] = zb_new;
       // ib += G^T(mbar z) (objective.py:160-161), gather form on q_c = mbar_c * z
-      auto q0 = [&](int jr) { return -res[jr * OP + i] * tz[jr * OX + i]; };
-      auto q1 = [&](int ic) { return -res[(OY + j) * OP + ic] * tz[j * OX + ic]; };
+      auto q0 = [&](int jr) { return -res[jr * OP + i] * tz[jr * OXP + i]; };
+      auto q1 = [&](int ic) { return -res[(OY + j) * OP + ic] * tz[j * OXP + ic]; };
       const T zc = tz[e];
       const T qc0 = m0 * zc, qc1 = m1 * zc;
       const T gm = (gy > 0) ? q0(j - 1) : T(0);

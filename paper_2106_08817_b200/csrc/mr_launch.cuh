@@ -8,7 +8,14 @@
 
 namespace mr {
 
-inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? MR_OK : MR_ECUDA; }
+// last CUDA error seen by a launcher on this thread (reported by mr_last_error)
+inline thread_local cudaError_t g_last_cuda = cudaSuccess;
+
+inline int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return MR_OK;
+  g_last_cuda = e;
+  return MR_ECUDA;
+}
 
 template <typename T>
 int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
