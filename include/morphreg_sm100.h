@@ -72,13 +72,14 @@ typedef struct {
 
 #define MR_MAX_RADIUS 32
 
-/* ---- single-step operators ------------------------------------------------ */
+/* ---- single-step operators (2D; mr_sl_step also 3D) ------------------------ */
 
 /* v = -K * (z grad I) for every pair.  Replaces velocity_from_momentum /
  * velocity_arr (integrator.py:93-94, 124-130), i.e. gradient_arr
  * (fields.py:161-162) + smooth_vec_arr (kernel.py:82-85).
- * guard: nullable int32[B]; OR-ed with MR_GUARD_* for I, z, v (_guard,
- * integrator.py:113-118). */
+ * guard: nullable int32[B]; OR-ed with the MR_GUARD_VELOCITY_* bits of v
+ * (_guard, integrator.py:113-118; mr_shoot_forward guards I and z in the
+ * transport step that produces them). */
 int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
                 void* v, int32_t* guard, void* stream);
 
@@ -109,15 +110,21 @@ int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I,
 
 /* ---- whole-loop entry points (one call per shoot / gradient) -------------- */
 
+/* Bytes of device workspace mr_shoot_forward needs (0 in 2D; 3 scalars per
+ * voxel in 3D, where the separable smoothing round-trips through it). */
+size_t mr_forward_workspace_bytes(int dtype, mr_grid g);
+
 /* shoot() for Scheme.SEMI_LAGRANGIAN (integrator.py:163-219), every pair of
- * the batch.  Trajectory buffers hold all n_steps+1 states:
+ * the batch, 2D or 3D (trilinear, 3-axis smoothing).  Trajectory buffers
+ * hold all n_steps+1 states:
  *   traj_I, traj_z: [T+1][B][N]; traj_v: [T+1][B][d][N];
  *   phi: nullable [B][d][N] final pull-back grid (SampleGrid);
  *   guard: nullable int32[B][T+1] (zero-filled by the library, then OR-ed).
  * traj_I[0], traj_z[0] must already hold I0, z0. dt = 1/n_steps. */
 int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu,
                      int32_t n_steps, void* traj_I, void* traj_z,
-                     void* traj_v, void* phi, int32_t* guard, void* stream);
+                     void* traj_v, void* phi, int32_t* guard, void* workspace,
+                     void* stream);
 
 /* Bytes of device workspace mr_shoot_adjoint needs for grid g. */
 size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g);

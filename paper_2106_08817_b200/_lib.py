@@ -38,6 +38,7 @@ EXPORTS = (
     "mr_sl_step_adjoint",
     "mr_velocity_adjoint",
     "mr_shoot_forward",
+    "mr_forward_workspace_bytes",
     "mr_adjoint_workspace_bytes",
     "mr_shoot_adjoint",
     "mr_cost_terms",
@@ -65,7 +66,8 @@ _SIGNATURES = {
     "mr_sl_step": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_sl_step_adjoint": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_velocity_adjoint": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "mr_shoot_forward": (_i32, [_i32, MrGrid, MrKernel, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_shoot_forward": (_i32, [_i32, MrGrid, MrKernel, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_forward_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
     "mr_adjoint_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
     "mr_shoot_adjoint": (
         _i32,

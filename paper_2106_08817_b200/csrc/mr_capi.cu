@@ -40,14 +40,21 @@ static int check_rc(int rc, const char* where) {
   return fail(rc, std::string(where) + ": invalid argument");
 }
 
-static int validate(int dtype, const mr_grid& g) {
+static int validate(int dtype, const mr_grid& g, bool allow3d = true) {
   if (dtype != MR_F32 && dtype != MR_F64) return fail(MR_EINVAL, "dtype must be MR_F32 or MR_F64");
-  if (g.ndim != 2) return fail(MR_EINVAL, "only ndim == 2 is supported by this build");
+  if (g.ndim != 2 && g.ndim != 3) return fail(MR_EINVAL, "ndim must be 2 or 3");
+  if (g.ndim == 3 && !allow3d)
+    return fail(MR_EINVAL, "3D: use the whole-loop entry points mr_shoot_forward/mr_shoot_adjoint");
   if (g.batch < 1) return fail(MR_EINVAL, "batch must be >= 1");
-  if (g.n[0] < 2 || g.n[1] < 2)
-    return fail(MR_EINVAL, "grid must be at least 2x2, got " + std::to_string(g.n[0]) + "x" +
-                               std::to_string(g.n[1]));
-  if ((long long)g.n[0] * g.n[1] > (1LL << 31) - 1) return fail(MR_EINVAL, "grid too large");
+  if (g.n[0] < 2 || g.n[1] < 2 || (g.ndim == 3 && g.n[2] < 2)) {
+    std::string dims = std::to_string(g.n[0]) + "x" + std::to_string(g.n[1]);
+    if (g.ndim == 3) dims += "x" + std::to_string(g.n[2]);
+    return fail(MR_EINVAL, "grid must be at least 2x2, got " + dims);
+  }
+  long long N = (long long)g.n[0] * g.n[1] * (g.ndim == 3 ? g.n[2] : 1);
+  if (N > (1LL << 31) - 1) return fail(MR_EINVAL, "grid too large");
+  if ((long long)g.batch * 3 * (g.ndim == 3 ? g.n[0] : 1) > 65535)
+    return fail(MR_EINVAL, "batch too large for one launch");
   return MR_OK;
 }
 
@@ -85,12 +92,62 @@ static int make_taps(const mr_kernel& k, Taps<T>& tp) {
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static Grid3 grid3(const mr_grid& g) {
+  Grid3 r;
+  r.B = g.batch;
+  r.D = g.n[0];
+  r.H = g.n[1];
+  r.W = g.n[2];
+  r.HW = (long long)r.H * r.W;
+  r.N = (long long)r.D * r.HW;
+  return r;
+}
+
+static long long scalars(const mr_grid& g) {
+  return (long long)g.batch * g.n[0] * g.n[1] * (g.ndim == 3 ? g.n[2] : 1);
+}
+
+static unsigned flat_blocks(long long n) {
+  long long b = (n + kThreads - 1) / kThreads;
+  return (unsigned)(b < 148LL * 16 ? b : 148LL * 16);
+}
+
+// ---- 3D building blocks ----------------------------------------------------------
+
+// v = -K*(z grad I): product -> per-slice FIR (axes 1, 2) -> axis-0 FIR (+negate, guard).
+// `v` doubles as the product scratch; `tmp` holds 3 scalars per voxel.
+template <typename T>
+static int velocity3d(const Grid3& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
+                      T* tmp, int32_t* guard, int guard_stride, cudaStream_t s) {
+  k_product3d<T><<<flat_blocks((long long)g.B * g.N), kThreads, 0, s>>>(I, z, v, g);
+  int rc = cuda_status(cudaGetLastError());
+  if (rc) return rc;
+  Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};  // every (pair, component, slice) as a 2D image
+  rc = launch_smooth2d<T>(sl, R, tp, v, tmp, false, s);
+  if (rc) return rc;
+  return launch_fir_axis0<T>(R, tp, tmp, v, g.B * 3, g.D, g.HW, false, 1, guard, guard_stride, s);
+}
+
+template <typename T>
+static int sl_step3d(const Grid3& g, double dt, double mu, const T* I, const T* z, const T* v,
+                     T* In, T* zn, const T* phi_in, T* phi_out, cudaStream_t s,
+                     int32_t* guard_in = nullptr, int32_t* guard_out = nullptr,
+                     int guard_stride = 1) {
+  Step3Args<T> a{I,       z,      v,        In,          zn,      phi_in,    phi_out,
+                 (T)dt,   (T)(dt * mu), mu != 0.0, guard_in, guard_out, guard_stride, g};
+  k_sl_step3d<T><<<flat_blocks((long long)g.B * g.N), kThreads, 0, s>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------------------------
 template <typename T>
 static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, const T* z,
                             const T* v, T* In, T* zn, const T* phi_in, T* phi_out,
-                            cudaStream_t s) {
-  StepArgs<T> a{I, z, v, In, zn, phi_in, phi_out, (T)dt, (T)(dt * mu), mu != 0.0, g};
+                            cudaStream_t s, int32_t* guard_in = nullptr,
+                            int32_t* guard_out = nullptr, int guard_stride = 1) {
+  StepArgs<T> a{I,     z,       v,      In,        zn,          phi_in,
+                phi_out, (T)dt, (T)(dt * mu), mu != 0.0, guard_in, guard_out,
+                guard_stride, g};
   dim3 grid((g.W + 31) / 32, (g.H + kThreads / 32 - 1) / (kThreads / 32), g.B);
   k_sl_step2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
@@ -122,11 +179,51 @@ static int launch_cost_terms2d(const Grid2& g, double lam, double rho, const T* 
 
 // ---------------------------------------------------------------------------------
 template <typename T>
+static int shoot_forward3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>& tp, double mu,
+                           int T_, T* I, T* z, T* v, void* phi, int32_t* guard, T* tmp,
+                           cudaStream_t s) {
+  const Grid3 g = grid3(mg);
+  const double dt = 1.0 / T_;
+  const long long S1 = (long long)g.B * g.N;
+  const long long SV = 3 * S1;
+  T* ph[2] = {nullptr, nullptr};
+  if (phi) {
+    T* base = static_cast<T*>(phi);
+    ph[0] = (T_ % 2 == 0) ? base : base + SV;
+    ph[1] = (T_ % 2 == 0) ? base + SV : base;
+    k_identity3d<T><<<592, 256, 0, s>>>(ph[0], g);
+  }
+  if (guard && cudaMemsetAsync(guard, 0, sizeof(int32_t) * (size_t)g.B * (T_ + 1), s) != cudaSuccess)
+    return check_cuda("memset guard");
+  int rc;
+  for (int step = 0; step < T_; ++step) {
+    rc = velocity3d<T>(g, k.radius, tp, I + step * S1, z + step * S1, v + step * SV, tmp,
+                       guard ? guard + step : nullptr, T_ + 1, s);
+    if (rc) return check_rc(rc, "velocity3d");
+    rc = sl_step3d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, I + (step + 1) * S1,
+                      z + (step + 1) * S1, ph[step & 1], ph[(step + 1) & 1], s,
+                      (guard && step == 0) ? guard : nullptr, guard ? guard + step + 1 : nullptr,
+                      T_ + 1);
+    if (rc) return check_rc(rc, "sl_step3d");
+  }
+  rc = velocity3d<T>(g, k.radius, tp, I + T_ * S1, z + T_ * S1, v + T_ * SV, tmp,
+                     guard ? guard + T_ : nullptr, T_ + 1, s);
+  if (rc) return check_rc(rc, "velocity3d");
+  return MR_OK;
+}
+
+template <typename T>
 static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T_, void* trI,
-                         void* trz, void* trv, void* phi, int32_t* guard, cudaStream_t s) {
+                         void* trz, void* trv, void* phi, int32_t* guard, void* ws,
+                         cudaStream_t s) {
   Taps<T> tp;
   int rc = make_taps<T>(k, tp);
   if (rc) return rc;
+  if (mg.ndim == 3) {
+    if (!ws) return fail(MR_EINVAL, "3D shoot needs a workspace (mr_forward_workspace_bytes)");
+    return shoot_forward3d<T>(mg, k, tp, mu, T_, static_cast<T*>(trI), static_cast<T*>(trz),
+                              static_cast<T*>(trv), phi, guard, static_cast<T*>(ws), s);
+  }
   const Grid2 g = grid2(mg);
   const double dt = 1.0 / T_;  // ShootingConfig.dt (integrator.py:67-69)
   T* I = static_cast<T*>(trI);
@@ -150,12 +247,99 @@ static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T
     if (rc) return check_rc(rc, "velocity");
     rc = launch_sl_step2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV,
                              I + (step + 1) * S1, z + (step + 1) * S1, ph[step & 1],
-                             ph[(step + 1) & 1], s);
+                             ph[(step + 1) & 1], s,
+                             (guard && step == 0) ? guard : nullptr,
+                             guard ? guard + step + 1 : nullptr, T_ + 1);
     if (rc) return check_rc(rc, "sl_step");
   }
   rc = launch_velocity2d<T>(g, k.radius, tp, I + T_ * S1, z + T_ * S1, v + T_ * SV,
                             guard ? guard + T_ : nullptr, T_ + 1, s);
   if (rc) return check_rc(rc, "velocity");
+  return MR_OK;
+}
+
+template <typename T>
+static int cost_terms3d(const Grid3& g, double lam, double rho, const T* I0, const T* z0,
+                        const T* v0, const T* IT, const T* J, double* terms, T* seed,
+                        cudaStream_t s) {
+  if (cudaMemsetAsync(terms, 0, sizeof(double) * 4 * g.B, s) != cudaSuccess) return MR_ECUDA;
+  long long blocks = (g.N + kThreads * 4 - 1) / (kThreads * 4);
+  if (blocks > 1024) blocks = 1024;
+  k_cost_terms3d<T><<<dim3((unsigned)blocks, g.B), kThreads, 0, s>>>(I0, z0, v0, IT, J, seed,
+                                                                      terms, g);
+  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, g.B, lam, rho);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>& tp, double mu,
+                           int T_, double lam, double rho, const T* I, const T* z, const T* v,
+                           const T* J, T* zbar0, double* terms, int32_t* flags, T* w,
+                           cudaStream_t s) {
+  const Grid3 g = grid3(mg);
+  const double dt = 1.0 / T_;
+  const long long S1 = (long long)g.B * g.N;
+  const long long SV = 3 * S1;
+  T* cur = w;              // ibar | zbar   (2*S1)
+  T* acc = w + 2 * S1;     // ib   | zb     (2*S1)
+  T* vbar = w + 4 * S1;    // 3*S1
+  T* tmp = w + 7 * S1;     // 3*S1
+  T* sbuf = w + 10 * S1;   // S1
+  Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};
+  if (cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)g.B, s) != cudaSuccess)
+    return check_cuda("memset flags");
+  int rc = cost_terms3d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
+  if (rc) return check_rc(rc, "cost_terms3d");
+  if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
+  const unsigned nb = flat_blocks(S1);
+  for (int step = T_ - 1; step >= 0; --step) {
+    if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
+    Adj3Args<T> a{};
+    a.I = I + step * S1;
+    a.z = z + step * S1;
+    a.v = v + step * SV;
+    a.ibar = cur;
+    a.zbar = cur + S1;
+    a.s = sbuf;
+    a.ib = acc;
+    a.zb = acc + S1;
+    a.vbar = vbar;
+    a.s_out = sbuf;
+    a.dt = (T)dt;
+    a.dtmu = (T)(dt * mu);
+    a.has_mu = mu != 0.0;
+    a.reg_lam = (T)(step == 0 ? lam : 0.0);
+    a.g = g;
+    k_divseed3d<T><<<nb, kThreads, 0, s>>>(a);
+    k_sl_adjoint3d<T><<<nb, kThreads, 0, s>>>(a);
+    if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "sl_adjoint3d");
+    // ktv = K^T vbar: axis 0 first, then axes 1, 2 per slice (kernel.py:76-79 order)
+    rc = launch_fir_axis0<T>(k.radius, tp, vbar, tmp, g.B * 3, g.D, g.HW, true, 0, nullptr, 1, s);
+    if (rc) return check_rc(rc, "fir_axis0^T");
+    rc = launch_smooth2d<T>(sl, k.radius, tp, tmp, vbar, true, s);
+    if (rc) return check_rc(rc, "smooth2d^T");
+    VelAdj3Args<T> e{};
+    e.I = a.I;
+    e.z = a.z;
+    e.ktv = vbar;
+    e.ib = acc;
+    e.zb = acc + S1;
+    e.lam = (T)lam;
+    e.two_rho = (T)(2.0 * rho);
+    e.g = g;
+    if (step == 0) {
+      e.v0 = v;
+      e.zout = zbar0;
+      e.flags = flags;
+      k_veladj_epi3d<T, true><<<nb, kThreads, 0, s>>>(e);
+    } else {
+      k_veladj_epi3d<T, false><<<nb, kThreads, 0, s>>>(e);
+    }
+    if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "veladj_epi3d");
+    T* t = cur;
+    cur = acc;
+    acc = t;
+  }
   return MR_OK;
 }
 
@@ -167,6 +351,11 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
   Taps<T> tp;
   int rc = make_taps<T>(k, tp);
   if (rc) return rc;
+  if (mg.ndim == 3)
+    return shoot_adjoint3d<T>(mg, k, tp, mu, T_, lam, rho, static_cast<const T*>(trI),
+                              static_cast<const T*>(trz), static_cast<const T*>(trv),
+                              static_cast<const T*>(Jv), static_cast<T*>(zbar0), terms, flags,
+                              static_cast<T*>(ws), s);
   const Grid2 g = grid2(mg);
   const double dt = 1.0 / T_;
   const T* I = static_cast<const T*>(trI);
@@ -238,7 +427,7 @@ const char* mr_strerror(int code) {
 
 int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z, void* v,
                 int32_t* guard, void* stream) {
-  int rc = validate(dtype, g);
+  int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!I || !z || !v) return fail(MR_EINVAL, "NULL field pointer");
   Grid2 g2 = grid2(g);
@@ -258,7 +447,7 @@ int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
 
 int mr_smooth(int dtype, mr_grid g, mr_kernel k, const void* a, void* out, int32_t adjoint,
               void* stream) {
-  int rc = validate(dtype, g);
+  int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!a || !out) return fail(MR_EINVAL, "NULL field pointer");
   Grid2 g2 = grid2(g);
@@ -284,6 +473,18 @@ int mr_sl_step(int dtype, mr_grid g, double dt, double mu, const void* I, const 
   if (!I || !z || !v || !I_next || !z_next) return fail(MR_EINVAL, "NULL field pointer");
   if ((phi_in == nullptr) != (phi_out == nullptr))
     return fail(MR_EINVAL, "phi_in and phi_out must both be set or both be NULL");
+  if (g.ndim == 3) {
+    Grid3 g3 = grid3(g);
+    rc = MR_DISPATCH(dtype,
+                     sl_step3d<float>(g3, dt, mu, (const float*)I, (const float*)z,
+                                      (const float*)v, (float*)I_next, (float*)z_next,
+                                      (const float*)phi_in, (float*)phi_out, as_stream(stream)),
+                     sl_step3d<double>(g3, dt, mu, (const double*)I, (const double*)z,
+                                       (const double*)v, (double*)I_next, (double*)z_next,
+                                       (const double*)phi_in, (double*)phi_out,
+                                       as_stream(stream)));
+    return check_rc(rc, "mr_sl_step");
+  }
   Grid2 g2 = grid2(g);
   rc = MR_DISPATCH(dtype,
                    launch_sl_step2d<float>(g2, dt, mu, (const float*)I, (const float*)z,
@@ -300,7 +501,7 @@ int mr_sl_step(int dtype, mr_grid g, double dt, double mu, const void* I, const 
 int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu, const void* I, const void* z,
                        const void* v, const void* ibar, const void* zbar, void* ib, void* zb,
                        void* vbar, void* stream) {
-  int rc = validate(dtype, g);
+  int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!I || !z || !v || !ibar || !zbar || !ib || !zb || !vbar)
     return fail(MR_EINVAL, "NULL field pointer");
@@ -318,7 +519,7 @@ int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu, const void* I
 
 int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
                         const void* vbar, void* ib, void* zb, void* stream) {
-  int rc = validate(dtype, g);
+  int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!I || !z || !vbar || !ib || !zb) return fail(MR_EINVAL, "NULL field pointer");
   Grid2 g2 = grid2(g);
@@ -340,9 +541,15 @@ int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const 
   return check_rc(rc, "mr_velocity_adjoint");
 }
 
+size_t mr_forward_workspace_bytes(int dtype, mr_grid g) {
+  if (validate(dtype, g)) return 0;
+  if (g.ndim == 2) return 0;
+  return (size_t)(dtype == MR_F32 ? 4 : 8) * (size_t)scalars(g) * 3;
+}
+
 int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps,
                      void* traj_I, void* traj_z, void* traj_v, void* phi, int32_t* guard,
-                     void* stream) {
+                     void* workspace, void* stream) {
   int rc = validate(dtype, g);
   if (rc) return rc;
   if (n_steps < 1) return fail(MR_EINVAL, "n_steps must be >= 1, got " + std::to_string(n_steps));
@@ -350,9 +557,9 @@ int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_ste
   if (!traj_I || !traj_z || !traj_v) return fail(MR_EINVAL, "NULL trajectory pointer");
   rc = MR_DISPATCH(dtype,
                    shoot_forward<float>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
-                                        as_stream(stream)),
+                                        workspace, as_stream(stream)),
                    shoot_forward<double>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
-                                         as_stream(stream)));
+                                         workspace, as_stream(stream)));
   if (rc) return rc;
   return check_cuda("mr_shoot_forward");
 }
@@ -360,8 +567,8 @@ int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_ste
 size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g) {
   if (validate(dtype, g)) return 0;
   size_t es = dtype == MR_F32 ? 4 : 8;
-  size_t S1 = (size_t)g.batch * (size_t)g.n[0] * (size_t)g.n[1];
-  return es * S1 * (4 + 2);
+  size_t S1 = (size_t)scalars(g);
+  return es * S1 * (g.ndim == 3 ? 11 : 6);
 }
 
 int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps, double lam,
@@ -390,6 +597,18 @@ int mr_cost_terms(int dtype, mr_grid g, double lam, double rho, const void* I0, 
   int rc = validate(dtype, g);
   if (rc) return rc;
   if (!I0 || !z0 || !v0 || !IT || !J || !terms) return fail(MR_EINVAL, "NULL pointer");
+  if (g.ndim == 3) {
+    Grid3 g3 = grid3(g);
+    rc = MR_DISPATCH(dtype,
+                     cost_terms3d<float>(g3, lam, rho, (const float*)I0, (const float*)z0,
+                                         (const float*)v0, (const float*)IT, (const float*)J,
+                                         terms, (float*)ibar_seed, as_stream(stream)),
+                     cost_terms3d<double>(g3, lam, rho, (const double*)I0, (const double*)z0,
+                                          (const double*)v0, (const double*)IT,
+                                          (const double*)J, terms, (double*)ibar_seed,
+                                          as_stream(stream)));
+    return check_rc(rc, "mr_cost_terms");
+  }
   Grid2 g2 = grid2(g);
   rc = MR_DISPATCH(dtype,
                    launch_cost_terms2d<float>(g2, lam, rho, (const float*)I0, (const float*)z0,

@@ -97,6 +97,36 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
   }
 }
 
+template <typename T, int R, bool TR, int EPI>
+int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
+                int32_t* guard, int guard_stride, cudaStream_t s) {
+  constexpr size_t bytes = Ax0Smem<T, R>::bytes;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      k_fir_axis0<T, R, TR, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (attr != cudaSuccess) return cuda_status(attr);
+  dim3 grid((unsigned)((HW + kAx0X - 1) / kAx0X), (unsigned)((D + kAx0D - 1) / kAx0D),
+            (unsigned)V);
+  k_fir_axis0<T, R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
+                                                            tp);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
+                     bool transpose, int epi, int32_t* guard, int guard_stride, cudaStream_t s) {
+  switch (R) {
+#define MR_CASE(RR)                                                                          \
+  case RR:                                                                                   \
+    if (transpose)                                                                           \
+      return fir_axis0_r<T, RR, true, 0>(tp, in, out, V, D, HW, guard, guard_stride, s);     \
+    if (epi) return fir_axis0_r<T, RR, false, 1>(tp, in, out, V, D, HW, guard, guard_stride, s); \
+    return fir_axis0_r<T, RR, false, 0>(tp, in, out, V, D, HW, guard, guard_stride, s);
+    MR_RADIUS_LIST(MR_CASE)
+#undef MR_CASE
+    default: return MR_EINVAL;
+  }
+}
+
 }  // namespace mr
 
 #define MR_INSTANTIATE_FIR(T)                                                                   \
@@ -107,4 +137,6 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
                                   cudaStream_t);                                                \
   template int launch_velocity_adj2d<T>(const Grid2&, int, const Taps<T>&,                      \
                                         const VelAdjArgs<T>&, bool, cudaStream_t);              \
+  template int launch_fir_axis0<T>(int, const Taps<T>&, const T*, T*, int, int, long long, bool, \
+                                   int, int32_t*, int, cudaStream_t);                           \
   }

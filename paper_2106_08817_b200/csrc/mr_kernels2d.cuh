@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kThreads)
   const int H = a.g.H, W = a.g.W;
   const int b = blockIdx.z;
   const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
+  unsigned flags = 0;
   const int offZ = align_shift(x_org - R, S::A), offI = align_shift(x_org - R - 1, S::A);
   T* rg = rg0 + offZ;  // region element (j, i) at rg[j*PX + i]
   T* m0 = rg;
@@ -298,8 +299,8 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
   }
 
-  // ---- m = z grad I at in-image region samples (integrator.py:94); guard I, z ----
-  unsigned flags = 0;
+  // ---- m = z grad I at in-image region samples (integrator.py:94) ----
+  // (the guard on I and z runs in the transport kernel that produces them)
   const int i_lo = max(0, R - x_org), i_hi = min(RX, W - x_org + R);  // in-image columns
   const int j_lo = max(0, R - y_org), j_hi = min(RY, H - y_org + R);  // in-image rows
   // interior tile: every in-image sample has both neighbours on both axes
@@ -307,7 +308,6 @@ __global__ void __launch_bounds__(kThreads)
                         (x_org - R + RX <= W - 1);
   for (int j = j_lo + warp; j < j_hi; j += kNW) {
     const int uy = y_org - R + j;
-    const bool own_row = j >= R && j < R + S::OY;
     const T* crow = ist + (j + 1) * PXI + 1;
     for (int i = i_lo + lane; i < i_hi; i += 32) {
       const T* c = crow + i;
@@ -325,23 +325,30 @@ __global__ void __launch_bounds__(kThreads)
       const T zz = m1[p];
       m0[p] = zz * g0;
       m1[p] = zz * g1;
-      if (own_row && i >= R && i < R + S::OX) {
-        flags |= guard_bits(f0, MR_GUARD_IMAGE_NONFINITE);
-        flags |= guard_bits(zz, MR_GUARD_MOMENTUM_NONFINITE);
-      }
     }
   }
   __syncthreads();
   // border tiles: replicate the border samples into the clamped halo
-  if (i_lo > 0 || j_lo > 0 || i_hi < RX || j_hi < RY) {
-    for (int j = warp; j < RY; j += kNW) {
-      const int jr = min(max(j, j_lo), j_hi - 1);
+  // (columns of in-image rows first, then whole rows)
+  if (i_lo > 0 || i_hi < RX) {
+    const int nl = i_lo, nr = RX - i_hi;
+    for (int j = j_lo + warp; j < j_hi; j += kNW)
+      for (int t = lane; t < nl + nr; t += 32) {
+        const int i = t < nl ? t : i_hi + (t - nl);
+        const int ir = t < nl ? i_lo : i_hi - 1;
+        m0[j * PX + i] = m0[j * PX + ir];
+        m1[j * PX + i] = m1[j * PX + ir];
+      }
+    __syncthreads();
+  }
+  if (j_lo > 0 || j_hi < RY) {
+    const int nt = j_lo, nb = RY - j_hi;
+    for (int t = warp; t < nt + nb; t += kNW) {
+      const int j = t < nt ? t : j_hi + (t - nt);
+      const int jr = t < nt ? j_lo : j_hi - 1;
       for (int i = lane; i < RX; i += 32) {
-        const int ir = min(max(i, i_lo), i_hi - 1);
-        if (jr != j || ir != i) {
-          m0[j * PX + i] = m0[jr * PX + ir];
-          m1[j * PX + i] = m1[jr * PX + ir];
-        }
+        m0[j * PX + i] = m0[jr * PX + i];
+        m1[j * PX + i] = m1[jr * PX + i];
       }
     }
     __syncthreads();
@@ -413,6 +420,9 @@ struct StepArgs {
   T* phi_out;
   T dt, dtmu;
   bool has_mu;
+  int32_t* guard_in;   // nullable: guard word of the input step (checked at step 0 only)
+  int32_t* guard_out;  // nullable: guard word of the output step
+  int guard_stride;
   Grid2 g;
 };
 
@@ -434,6 +444,11 @@ __global__ void __launch_bounds__(kThreads) k_sl_step2d(StepArgs<T> a) {
   const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
   const long long c00 = (long long)py.i0 * W + px.i0;
   const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
+  if (a.guard_in) {  // _guard(0, image, momentum) on the inputs (integrator.py:184)
+    const unsigned fin = guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE) |
+                         guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
+    if (fin) atomicOr(reinterpret_cast<int*>(a.guard_in + (long long)b * a.guard_stride), (int)fin);
+  }
   T bi = bilerp(I[c00], I[c10], I[c01], I[c11], py.f, px.f);
   if (a.has_mu) bi = bi + a.dtmu * z[q];  // advect_image_sl_arr: + dt*mu*z
   const T bz = bilerp(z[c00], z[c10], z[c01], z[c11], py.f, px.f);
@@ -443,8 +458,15 @@ __global__ void __launch_bounds__(kThreads) k_sl_step2d(StepArgs<T> a) {
   const T lf = (x > 0) ? v1[q - 1] : vx;
   const T rt = (x < W - 1) ? v1[q + 1] : vx;
   const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
+  const T zn = bz * (T(1) - a.dt * div);
   a.In[b * N + q] = bi;
-  a.zn[b * N + q] = bz * (T(1) - a.dt * div);
+  a.zn[b * N + q] = zn;
+  if (a.guard_out) {  // flags are almost always zero: no warp reduction needed
+    const unsigned fout = guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) |
+                          guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+    if (fout)
+      atomicOr(reinterpret_cast<int*>(a.guard_out + (long long)b * a.guard_stride), (int)fout);
+  }
   if (a.phi_in) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {

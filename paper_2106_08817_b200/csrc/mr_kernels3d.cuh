@@ -1,0 +1,547 @@
+// mr_kernels3d.cuh -- 3D kernels of the semi-Lagrangian shooting path.
+//
+// The reference is 2D only; the 3D operators restate it per axis
+// exactly as the N-D oracle does (oracle/morphreg_oracle.py): np.gradient per
+// axis, its exact transpose, trilinear interpolation with the reference clamp
+// and strict inside masks, separable replicate-border Gaussian over 3 axes.
+// Layout: scalar [B][D][H][W], vector [B][3][D][H][W]; axis 0 = D.
+//
+// Velocity  v = -K*(z grad I):   k_product3d -> per-slice 2D FIR (axes 1, 2;
+//                                k_smooth2d tile engine) -> k_fir_axis0 (+negate, guard)
+// Transport (trilinear):         k_sl_step3d
+// Transport adjoint:             k_divseed3d (s = -dt zbar B(z)) -> k_sl_adjoint3d
+// Velocity adjoint:              k_fir_axis0^T -> per-slice 2D FIR^T -> k_veladj_epi3d
+// Cost terms:                    k_cost_terms3d
+#pragma once
+
+#include "mr_kernels2d.cuh"
+
+namespace mr {
+
+struct Grid3 {
+  int B, D, H, W;
+  long long N;   // D*H*W
+  long long HW;  // H*W
+};
+
+__device__ __forceinline__ void coords3(long long q, const Grid3& g, int& d, int& y, int& x) {
+  d = (int)(q / g.HW);
+  long long r = q - (long long)d * g.HW;
+  y = (int)(r / g.W);
+  x = (int)(r - (long long)y * g.W);
+}
+
+// np.gradient of f at (d, y, x) along the three axes.
+template <typename T>
+__device__ __forceinline__ void grad3(const T* __restrict__ f, long long q, int d, int y, int x,
+                                      const Grid3& g, T& g0, T& g1, T& g2) {
+  const T c = f[q];
+  const long long HW = g.HW;
+  g0 = grad1(d > 0 ? f[q - HW] : c, c, d < g.D - 1 ? f[q + HW] : c, d, g.D);
+  g1 = grad1(y > 0 ? f[q - g.W] : c, c, y < g.H - 1 ? f[q + g.W] : c, y, g.H);
+  g2 = grad1(x > 0 ? f[q - 1] : c, c, x < g.W - 1 ? f[q + 1] : c, x, g.W);
+}
+
+// ------------------------------------------------------------------------------
+// m_c = z * d_c I  (integrator.py:94 per axis) -> out [B][3][N]
+// ------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_product3d(const T* __restrict__ I,
+                                                         const T* __restrict__ z, T* out,
+                                                         Grid3 g) {
+  const long long total = (long long)g.B * g.N;
+  for (long long p = blockIdx.x * (long long)kThreads + threadIdx.x; p < total;
+       p += (long long)gridDim.x * kThreads) {
+    const long long b = p / g.N, q = p - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    T g0, g1, g2;
+    grad3(I + b * g.N, q, d, y, x, g, g0, g1, g2);
+    const T zz = z[p];
+    T* o = out + b * 3 * g.N + q;
+    o[0] = zz * g0;
+    o[g.N] = zz * g1;
+    o[2 * g.N] = zz * g2;
+  }
+}
+
+// ------------------------------------------------------------------------------
+// 1D FIR along axis 0 of a stack of volumes [V][D][HW] (V = B*3):
+//  forward: replicate borders (conv1d_replicate, kernel.py:36-45)
+//  transpose: exact transpose (kernel.py:48-68): zero padding + edge rows.
+// Tile: 64 consecutive HW elements x OD outputs along D, halo R, register
+// blocking kRB outputs per thread.  EPI = 1: out = -acc with the velocity
+// guard (per pair b = volume / 3).
+// ------------------------------------------------------------------------------
+constexpr int kAx0X = 64, kAx0D = 32;
+
+template <typename T, int R>
+struct Ax0Smem {
+  static constexpr int RD = kAx0D + 2 * R;
+  static constexpr size_t bytes = sizeof(T) * (size_t)RD * kAx0X;
+};
+
+template <typename T, int R, bool TRANSPOSE, int EPI>
+__global__ void __launch_bounds__(kThreads)
+    k_fir_axis0(const T* __restrict__ in, T* out, int D, long long HW, int32_t* guard,
+                int guard_stride, Taps<T> tp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* rg = reinterpret_cast<T*>(smem_raw);
+  constexpr int RD = kAx0D + 2 * R;
+  const long long x0 = (long long)blockIdx.x * kAx0X;
+  const int d_org = blockIdx.y * kAx0D;
+  const int vol = blockIdx.z;
+  const T* __restrict__ src = in + (long long)vol * D * HW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < RD; j += kNW) {
+    int gd = d_org - R + j;
+    bool rin = true;
+    if (TRANSPOSE) {
+      rin = gd >= 0 && gd < D;
+      gd = rin ? gd : 0;
+    } else {
+      gd = min(max(gd, 0), D - 1);
+    }
+    const T* row = src + (long long)gd * HW;
+    for (int i = lane; i < kAx0X; i += 32) {
+      const long long gx = x0 + i;
+      const bool in_ = rin && gx < HW;
+      cp_async_elem_zfill(rg + j * kAx0X + i, row + (in_ ? gx : 0), in_);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+
+  constexpr int NB = kAx0D / kRB;
+  unsigned flags = 0;
+  for (int cb = warp; cb < NB; cb += kNW)
+    for (int i = lane; i < kAx0X; i += 32) {
+      const T* s = rg + cb * kRB * kAx0X + i;
+      T acc[kRB];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const T xv = s[t * kAx0X];
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], xv, acc[o]);
+        }
+      }
+      const int gd0 = d_org + cb * kRB;
+      if (TRANSPOSE) {
+        if (gd0 <= 0 && gd0 + kRB > 0) {
+          const int o = -gd0;
+          T a = T(0);
+#pragma unroll
+          for (int dd = 0; dd <= R; ++dd) a = fma(tp.e[R - dd], s[(o + R + dd) * kAx0X], a);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = a;
+        }
+        if (gd0 <= D - 1 && gd0 + kRB > D - 1) {
+          const int o = D - 1 - gd0;
+          T a = T(0);
+#pragma unroll
+          for (int dd = -R; dd <= 0; ++dd) a = fma(tp.e[R + dd], s[(o + R + dd) * kAx0X], a);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = a;
+        }
+      }
+      const long long gx = x0 + i;
+      if (gx >= HW) continue;
+      T* dst = out + (long long)vol * D * HW + gx;
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        const int gd = gd0 + o;
+        if (gd < D) {
+          T val = acc[o];
+          if (EPI == 1) {
+            val = -val;
+            flags |= guard_bits(val, MR_GUARD_VELOCITY_NONFINITE);
+          }
+          dst[(long long)gd * HW] = val;
+        }
+      }
+    }
+  if (EPI == 1 && guard && flags)
+    atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / 3) * guard_stride), (int)flags);
+}
+
+// ------------------------------------------------------------------------------
+// Trilinear plan / interpolation (fields.py:207-262 generalised; corner c has
+// offset bit ax = (c >> ax) & 1, weights multiplied in axis order).
+// ------------------------------------------------------------------------------
+template <typename T>
+struct Plan3 {
+  AxisPlan<T> a[3];
+  long long base;
+};
+
+template <typename T>
+__device__ __forceinline__ Plan3<T> plan3(int d, int y, int x, T v0, T v1, T v2, T dt,
+                                          const Grid3& g) {
+  Plan3<T> p;
+  p.a[0] = plan_axis<T>(d, v0, dt, g.D);
+  p.a[1] = plan_axis<T>(y, v1, dt, g.H);
+  p.a[2] = plan_axis<T>(x, v2, dt, g.W);
+  p.base = (long long)p.a[0].i0 * g.HW + (long long)p.a[1].i0 * g.W + p.a[2].i0;
+  return p;
+}
+
+template <typename T>
+__device__ __forceinline__ long long corner_off(int c, const Grid3& g) {
+  return ((c & 1) ? g.HW : 0) + ((c & 2) ? g.W : 0) + ((c & 4) ? 1 : 0);
+}
+
+template <typename T>
+__device__ __forceinline__ T axis_w(const Plan3<T>& p, int c, int ax) {
+  return ((c >> ax) & 1) ? p.a[ax].f : T(1) - p.a[ax].f;
+}
+
+template <typename T>
+__device__ __forceinline__ void corners8(const T* __restrict__ f, const Plan3<T>& p,
+                                         const Grid3& g, T v[8]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = f[p.base + corner_off<T>(c, g)];
+}
+
+template <typename T>
+__device__ __forceinline__ T trilerp(const T v[8], const Plan3<T>& p) {
+  T acc = T(0);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const T w = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
+    acc = (c == 0) ? w * v[c] : acc + w * v[c];
+  }
+  return acc;
+}
+
+// d(value)/d(coord_ax) * strict inside mask (interp_coord_grad of the oracle)
+template <typename T>
+__device__ __forceinline__ void coord_grad3(const T v[8], const Plan3<T>& p, T out[3]) {
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    T acc = T(0);
+    bool first = true;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if ((c >> ax) & 1) continue;
+      const int hi = c | (1 << ax);
+      T w = T(1);
+      bool has = false;
+#pragma unroll
+      for (int o = 0; o < 3; ++o) {
+        if (o == ax) continue;
+        w = has ? w * axis_w(p, c, o) : axis_w(p, c, o);
+        has = true;
+      }
+      const T t = w * (v[hi] - v[c]);
+      acc = first ? t : acc + t;
+      first = false;
+    }
+    out[ax] = acc * (p.a[ax].inside ? T(1) : T(0));
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K2 (3D): one SL step (integrator.py:101-110, 193-205)
+// ------------------------------------------------------------------------------
+template <typename T>
+struct Step3Args {
+  const T* I;
+  const T* z;
+  const T* v;
+  T* In;
+  T* zn;
+  const T* phi_in;
+  T* phi_out;
+  T dt, dtmu;
+  bool has_mu;
+  int32_t* guard_in;
+  int32_t* guard_out;
+  int guard_stride;
+  Grid3 g;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sl_step3d(Step3Args<T> a) {
+  const Grid3 g = a.g;
+  const long long total = (long long)g.B * g.N;
+  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
+       pp += (long long)gridDim.x * kThreads) {
+    const long long b = pp / g.N, q = pp - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    const T* __restrict__ I = a.I + b * g.N;
+    const T* __restrict__ z = a.z + b * g.N;
+    const T* __restrict__ v0 = a.v + b * 3 * g.N;
+    const T* __restrict__ v1 = v0 + g.N;
+    const T* __restrict__ v2 = v1 + g.N;
+    const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
+    const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
+    if (a.guard_in) {
+      const unsigned fin = guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE) |
+                           guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
+      if (fin) atomicOr(reinterpret_cast<int*>(a.guard_in + b * a.guard_stride), (int)fin);
+    }
+    T cv[8];
+    corners8(I, p, g, cv);
+    T bi = trilerp(cv, p);
+    if (a.has_mu) bi = bi + a.dtmu * z[q];
+    corners8(z, p, g, cv);
+    const T bz = trilerp(cv, p);
+    const T div = grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
+                  grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
+                  grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
+    const T zn = bz * (T(1) - a.dt * div);
+    a.In[pp] = bi;
+    a.zn[pp] = zn;
+    if (a.guard_out) {
+      const unsigned fo = guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) |
+                          guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+      if (fo) atomicOr(reinterpret_cast<int*>(a.guard_out + b * a.guard_stride), (int)fo);
+    }
+    if (a.phi_in) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        corners8(a.phi_in + (b * 3 + c) * g.N, p, g, cv);
+        a.phi_out[(b * 3 + c) * g.N + q] = trilerp(cv, p);
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_identity3d(T* phi, Grid3 g) {
+  const long long total = (long long)g.B * g.N;
+  for (long long pp = blockIdx.x * (long long)blockDim.x + threadIdx.x; pp < total;
+       pp += (long long)gridDim.x * blockDim.x) {
+    const long long b = pp / g.N, q = pp - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    phi[(b * 3 + 0) * g.N + q] = T(d);
+    phi[(b * 3 + 1) * g.N + q] = T(y);
+    phi[(b * 3 + 2) * g.N + q] = T(x);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K3 (3D): transport adjoint.  k_divseed3d writes s = -dt * zbar * B(z)
+// (objective.py:145); k_sl_adjoint3d does the scatters, the coordinate
+// gradients and vbar_c += D_c^T s (objective.py:128-147).
+// ------------------------------------------------------------------------------
+template <typename T>
+struct Adj3Args {
+  const T* I;
+  const T* z;
+  const T* v;
+  const T* ibar;
+  const T* zbar;
+  const T* s;  // divergence-adjoint seed
+  T* ib;
+  T* zb;
+  T* vbar;     // [B][3][N]
+  T* s_out;    // k_divseed3d output
+  T dt, dtmu;
+  bool has_mu;
+  T reg_lam;
+  Grid3 g;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_divseed3d(Adj3Args<T> a) {
+  const Grid3 g = a.g;
+  const long long total = (long long)g.B * g.N;
+  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
+       pp += (long long)gridDim.x * kThreads) {
+    const long long b = pp / g.N, q = pp - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    const T* __restrict__ v0 = a.v + b * 3 * g.N;
+    const Plan3<T> p = plan3<T>(d, y, x, v0[q], v0[g.N + q], v0[2 * g.N + q], a.dt, g);
+    T cv[8];
+    corners8(a.z + b * g.N, p, g, cv);
+    a.s_out[pp] = -a.dt * (a.zbar[pp] * trilerp(cv, p));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
+  const Grid3 g = a.g;
+  const long long total = (long long)g.B * g.N;
+  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
+       pp += (long long)gridDim.x * kThreads) {
+    const long long b = pp / g.N, q = pp - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    const T* __restrict__ I = a.I + b * g.N;
+    const T* __restrict__ z = a.z + b * g.N;
+    const T* __restrict__ v0 = a.v + b * 3 * g.N;
+    const T* __restrict__ v1 = v0 + g.N;
+    const T* __restrict__ v2 = v1 + g.N;
+    const T* __restrict__ s = a.s + b * g.N;
+    const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
+    const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
+    const T ib_ = a.ibar[pp], zb_ = a.zbar[pp];
+    T* __restrict__ ibo = a.ib + b * g.N;
+    T* __restrict__ zbo = a.zb + b * g.N;
+    T w8[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w8[c] = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) atomicAdd(ibo + p.base + corner_off<T>(c, g), w8[c] * ib_);
+    T cv[8], dI[3], dz[3];
+    corners8(I, p, g, cv);
+    coord_grad3(cv, p, dI);
+    T vb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
+    const T div =
+        grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
+        grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
+        grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
+    const T wz = zb_ * (T(1) - a.dt * div);
+    if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) atomicAdd(zbo + p.base + corner_off<T>(c, g), w8[c] * wz);
+    corners8(z, p, g, cv);
+    coord_grad3(cv, p, dz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
+    // vbar_c += D_c^T s (gather form along each axis)
+    {
+      const long long st[3] = {g.HW, (long long)g.W, 1};
+      const int pos[3] = {d, y, x};
+      const int n[3] = {g.D, g.H, g.W};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int j = pos[c];
+        const T sm = j > 0 ? s[q - st[c]] : T(0);
+        const T sp = j < n[c] - 1 ? s[q + st[c]] : T(0);
+        const T sf = j == 0 ? s[q] : (j == 1 ? sm : T(0));
+        const T sl = j == n[c] - 1 ? s[q] : (j == n[c] - 2 ? sp : T(0));
+        vb[c] += diff_adj1(sm, sp, sf, sl, j, n[c]);
+      }
+    }
+    if (a.reg_lam != T(0)) {
+      T g0, g1, g2;
+      grad3(I, q, d, y, x, g, g0, g1, g2);
+      const T zz = z[q];
+      vb[0] = vb[0] - a.reg_lam * (zz * g0);
+      vb[1] = vb[1] - a.reg_lam * (zz * g1);
+      vb[2] = vb[2] - a.reg_lam * (zz * g2);
+    }
+    T* vo = a.vbar + b * 3 * g.N + q;
+    vo[0] = vb[0];
+    vo[g.N] = vb[1];
+    vo[2 * g.N] = vb[2];
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K4 epilogue (3D): ktv = K^T vbar (so mbar = -ktv);
+//   zb += mbar . grad I;  ib += G^T(mbar z)  (objective.py:157-161)
+//   REG (k = 0): zout = zb + mbar.grad I0 + lam (K m0 . grad I0 + 2 rho z0), K m0 = -v0
+// ------------------------------------------------------------------------------
+template <typename T>
+struct VelAdj3Args {
+  const T* I;
+  const T* z;
+  const T* ktv;  // [B][3][N]
+  T* ib;
+  T* zb;
+  const T* v0;
+  T* zout;
+  int32_t* flags;
+  T lam, two_rho;
+  Grid3 g;
+};
+
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kThreads) k_veladj_epi3d(VelAdj3Args<T> a) {
+  const Grid3 g = a.g;
+  const long long total = (long long)g.B * g.N;
+  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
+       pp += (long long)gridDim.x * kThreads) {
+    const long long b = pp / g.N, q = pp - b * g.N;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    const T* __restrict__ I = a.I + b * g.N;
+    const T* __restrict__ z = a.z + b * g.N;
+    const T* __restrict__ kt = a.ktv + b * 3 * g.N;
+    T gr[3];
+    grad3(I, q, d, y, x, g, gr[0], gr[1], gr[2]);
+    const T m0 = -kt[q], m1 = -kt[g.N + q], m2 = -kt[2 * g.N + q];
+    T zb_new = a.zb[pp] + (m0 * gr[0] + m1 * gr[1] + m2 * gr[2]);
+    if (REG) {
+      const T* __restrict__ w = a.v0 + b * 3 * g.N;
+      const T km = -(w[q] * gr[0] + w[g.N + q] * gr[1] + w[2 * g.N + q] * gr[2]);
+      zb_new = zb_new + a.lam * (km + a.two_rho * z[q]);
+      a.zout[pp] = zb_new;
+      if (!isfinite(zb_new)) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+    } else {
+      a.zb[pp] = zb_new;
+      const long long st[3] = {g.HW, (long long)g.W, 1};
+      const int pos[3] = {d, y, x};
+      const int n[3] = {g.D, g.H, g.W};
+      T acc = T(0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T* kc = kt + c * g.N;
+        auto qv = [&](long long qq) { return -kc[qq] * z[qq]; };
+        const int j = pos[c];
+        const T qc = qv(q);
+        const T gm = j > 0 ? qv(q - st[c]) : T(0);
+        const T gp = j < n[c] - 1 ? qv(q + st[c]) : T(0);
+        const T gf = j == 0 ? qc : (j == 1 ? gm : T(0));
+        const T gl = j == n[c] - 1 ? qc : (j == n[c] - 2 ? gp : T(0));
+        const T t = diff_adj1(gm, gp, gf, gl, j, n[c]);
+        acc = (c == 0) ? t : acc + t;
+      }
+      a.ib[pp] = a.ib[pp] + acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K5 (3D): cost terms
+// ------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_cost_terms3d(const T* __restrict__ I0,
+                                                            const T* __restrict__ z0,
+                                                            const T* __restrict__ v0,
+                                                            const T* __restrict__ IT,
+                                                            const T* __restrict__ J, T* seed,
+                                                            double* terms, Grid3 g) {
+  __shared__ double red[kThreads / 32];
+  const int b = blockIdx.y;
+  const T* Ib = I0 + b * g.N;
+  const T* zb = z0 + b * g.N;
+  const T* vb = v0 + b * 3 * g.N;
+  double data = 0.0, vn = 0.0, zn = 0.0;
+  for (long long q = blockIdx.x * (long long)kThreads + threadIdx.x; q < g.N;
+       q += (long long)gridDim.x * kThreads) {
+    const T diff = IT[b * g.N + q] - J[b * g.N + q];
+    if (seed) seed[b * g.N + q] = diff;
+    data += (double)diff * (double)diff;
+    int d, y, x;
+    coords3(q, g, d, y, x);
+    T g0, g1, g2;
+    grad3(Ib, q, d, y, x, g, g0, g1, g2);
+    const T zz = zb[q];
+    vn += (double)(zz * g0) * (double)vb[q] + (double)(zz * g1) * (double)vb[g.N + q] +
+          (double)(zz * g2) * (double)vb[2 * g.N + q];
+    zn += (double)zz * (double)zz;
+  }
+  double s;
+  s = block_sum(data, red);
+  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 1], 0.5 * s);
+  s = block_sum(vn, red);
+  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 2], -s);
+  s = block_sum(zn, red);
+  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 3], s);
+}
+
+}  // namespace mr

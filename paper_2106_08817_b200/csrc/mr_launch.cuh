@@ -5,6 +5,7 @@
 #pragma once
 
 #include "mr_kernels2d.cuh"
+#include "mr_kernels3d.cuh"
 
 namespace mr {
 
@@ -26,5 +27,11 @@ int launch_smooth2d(const Grid2& g, int R, const Taps<T>& tp, const T* a, T* out
 template <typename T>
 int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdjArgs<T>& args,
                           bool reg, cudaStream_t s);
+
+// 1D FIR along axis 0 of V volumes [V][D][HW] (3D velocity / its adjoint);
+// epi = 1: negate + velocity guard (guard word of pair vol/3).
+template <typename T>
+int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
+                     bool transpose, int epi, int32_t* guard, int guard_stride, cudaStream_t s);
 
 }  // namespace mr

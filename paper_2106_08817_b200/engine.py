@@ -41,6 +41,7 @@ class DeviceTrajectory:
     v: torch.Tensor      # [T+1, B, d, *shape]
     guard: torch.Tensor  # int32 [B, T+1]
     phi: torch.Tensor | None = None  # [B, d, *shape] (first half of a 2x buffer)
+    workspace: torch.Tensor | None = None  # forward scratch (3D smoothing)
 
     @property
     def n_steps(self) -> int:
@@ -66,7 +67,12 @@ def allocate_trajectory(batch, shape, n_steps, dtype=torch.float32, device=None,
     phi = None
     if with_phi:
         phi = torch.empty((2, batch, d) + tuple(shape), dtype=dtype, device=device)
-    return DeviceTrajectory(I, z, v, guard, phi)
+    lib = _lib.load_library()
+    nbytes = lib.mr_forward_workspace_bytes(_lib.dtype_code(dtype), _lib.make_grid(batch, shape))
+    ws = None
+    if nbytes:
+        ws = torch.empty(nbytes // (torch.finfo(dtype).bits // 8), dtype=dtype, device=device)
+    return DeviceTrajectory(I, z, v, guard, phi, ws)
 
 
 def shoot_forward(traj: DeviceTrajectory, mu: float, weights, stream=None) -> DeviceTrajectory:
@@ -81,7 +87,8 @@ def shoot_forward(traj: DeviceTrajectory, mu: float, weights, stream=None) -> De
     g = _lib.make_grid(traj.batch, traj.shape)
     rc = lib.mr_shoot_forward(
         dt, g, kern.struct, float(mu), int(traj.n_steps), _lib.ptr(traj.I), _lib.ptr(traj.z),
-        _lib.ptr(traj.v), _lib.ptr(traj.phi), _lib.ptr(traj.guard), _lib.stream_ptr(stream),
+        _lib.ptr(traj.v), _lib.ptr(traj.phi), _lib.ptr(traj.guard), _lib.ptr(traj.workspace),
+        _lib.stream_ptr(stream),
     )
     _lib.check(rc)
     return traj
@@ -273,5 +280,9 @@ class BatchGrad:
         return self.bufs
 
     def launches_per_run(self) -> int:
-        """Kernels of ours per run(): forward 2T+1, adjoint cost+finalize + 2T."""
-        return (2 * self.n_steps + 1) + (2 + 2 * self.n_steps)
+        """Kernels of ours per run() (memsets excluded)."""
+        T = self.n_steps
+        if len(self.traj.shape) == 2:  # forward 2T+1; adjoint cost+finalize + 2T
+            return (2 * T + 1) + (2 + 2 * T)
+        # 3D: velocity = 3 kernels, step 1; adjoint: 2 + (2 + 2 FIR + 1) per step
+        return (3 * (T + 1) + T) + (2 + 5 * T)
