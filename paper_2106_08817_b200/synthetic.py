@@ -259,7 +259,7 @@ def make_config(idx: int, seed: int = 0, batch: int | None = None, pairs=None,
     if pairs is None:
         pairs = list(range(batch if batch is not None else spec["batch"]))
     manifest = {"config": idx, "seed": seed, "pairs": list(pairs), "shape": list(shp),
-                "ambiguities": "SURVEY.md Appendix C"}
+                "ambiguities": "SURVEY.md Appendix C", "offset_nominal": spec.get("offset")}
     if idx not in CONFIGS:
         raise ValueError(f"unknown config {idx}")
 
