@@ -2,6 +2,7 @@
 #pragma once
 
 #include "mr_launch.cuh"
+#include "mr_stream2d.cuh"
 #include "mr_tma.h"
 
 namespace mr {
@@ -10,8 +11,35 @@ inline dim3 fir_grid(int W, int H, int B, int tx, int ty) {
   return dim3((unsigned)((W + tx - 1) / tx), (unsigned)((H + ty - 1) / ty), (unsigned)B);
 }
 
+// Column-strip streaming kernel (fp32, TMA-describable layouts); returns 1 when
+// not applicable so the caller falls back to the tile kernel.
+template <typename T, int R>
+int velocity_stream_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
+  if constexpr (sizeof(T) != 4) {
+    return 1;  // fp64 (parity path) keeps the tile kernel
+  } else {
+  using C = StreamCfg<T, R>;
+  if (C::bytes > 227 * 1024) return 1;
+  CUtensorMap mI, mZ;
+  if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, C::PXI, C::G + 2) ||
+      !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, C::PXZ, C::G))
+    return 1;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      k_velocity2d_stream<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
+  if (attr != cudaSuccess) return cuda_status(attr);
+  a.use_tma = 1;
+  dim3 grid((unsigned)((g.W + C::OX - 1) / C::OX), (unsigned)g.B);
+  k_velocity2d_stream<T, R><<<grid, kThreads, C::bytes, s>>>(a, tp, mI, mZ);
+  return cuda_status(cudaGetLastError());
+  }
+}
+
 template <typename T, int R>
 int velocity_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
+  {
+    int rc = velocity_stream_r<T, R>(g, tp, a, s);
+    if (rc != 1) return rc;
+  }
   using S = FirSmem<T, R, 2>;
   using V = VelSmem<T, R>;
   constexpr size_t bytes = V::bytes;
