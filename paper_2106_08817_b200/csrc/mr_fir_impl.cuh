@@ -65,7 +65,42 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
 }
 
 template <typename T, int R, bool REG>
+int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
+  // Measured on B200 (cfg2): 0.41 ms vs 0.38 ms for the tile kernel, which
+  // overlaps all epilogue operand loads with pass 2.  Kept for future tuning.
+  constexpr bool kEnabled = false;
+  if constexpr (sizeof(T) != 4 || !kEnabled) {
+    return 1;
+  } else {
+    using C = StreamAdjCfg<T, R>;
+    constexpr size_t bytes = REG ? C::bytes_reg : C::bytes_noreg;
+    if (bytes > 227 * 1024) return 1;
+    VelAdjMaps m;
+    const long long B2 = 2LL * g.B;
+    const bool ok = make_map3<T>(&m.vbar, a.vbar, g.W, g.H, B2, C::PXZ, C::G) &&
+                    make_map3<T>(&m.I, a.I, g.W, g.H, g.B, C::OXP, C::G) &&
+                    make_map3<T>(&m.z, a.z, g.W, g.H, g.B, C::OXP, C::G) &&
+                    (REG ? make_map3<T>(&m.op2, a.v0, g.W, g.H, B2, C::OXP, C::G)
+                         : make_map3<T>(&m.op2, a.ib, g.W, g.H, g.B, C::OXP, C::G)) &&
+                    make_map3<T>(&m.zb, a.zb, g.W, g.H, g.B, C::OXP, C::G);
+    if (!ok) return 1;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_velocity_adj2d_stream<T, R, REG>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (attr != cudaSuccess) return cuda_status(attr);
+    a.use_tma = 1;
+    dim3 grid((unsigned)((g.W + C::OX - 3) / (C::OX - 2)), (unsigned)g.B);
+    k_velocity_adj2d_stream<T, R, REG><<<grid, kAdjStreamThreads, bytes, s>>>(a, tp, m);
+    return cuda_status(cudaGetLastError());
+  }
+}
+
+template <typename T, int R, bool REG>
 int veladj_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
+  {
+    int rc = veladj_stream_r<T, R, REG>(g, tp, a, s);
+    if (rc != 1) return rc;
+  }
   using S = FirSmem<T, R, 2>;
   using V = VelAdjSmem<T, R>;
   constexpr size_t bytes = VelAdjSmem<T, R>::bytes;

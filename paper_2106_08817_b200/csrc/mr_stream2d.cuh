@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(kThreads)
 
   // in-image input columns of the strip window
   const int i_lo = max(0, -xs), i_hi = min(RX, W - xs);
+  // every in-image column has both x neighbours in the image
+  const bool x_interior = (xs + i_lo >= 1) && (xs + i_hi - 1 <= W - 2);
 
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -107,14 +109,24 @@ __global__ void __launch_bounds__(kThreads)
           const T* zrow = zst + r * PXZ;
           T* p0 = P + r * PP;
           T* p1 = P + G * PP + r * PP;
-          for (int i = i_lo + lane; i < i_hi; i += 32) {
-            const T* c = crow + i;
-            const T f0 = c[0];
-            const T g0 = grad1(c[-PXI], f0, c[PXI], u, H);
-            const T g1 = grad1(c[-1], f0, c[1], xs + i, W);
-            const T zz = zrow[i];
-            p0[i] = zz * g0;
-            p1[i] = zz * g1;
+          const bool yin = u > 0 && u < H - 1;  // warp-uniform
+          if (yin && x_interior) {              // branch-free central differences
+            for (int i = i_lo + lane; i < i_hi; i += 32) {
+              const T* c = crow + i;
+              const T zz = zrow[i];
+              p0[i] = zz * ((c[PXI] - c[-PXI]) / T(2));
+              p1[i] = zz * ((c[1] - c[-1]) / T(2));
+            }
+          } else {
+            for (int i = i_lo + lane; i < i_hi; i += 32) {
+              const T* c = crow + i;
+              const T f0 = c[0];
+              const T g0 = grad1(c[-PXI], f0, c[PXI], u, H);
+              const T g1 = grad1(c[-1], f0, c[1], xs + i, W);
+              const T zz = zrow[i];
+              p0[i] = zz * g0;
+              p1[i] = zz * g1;
+            }
           }
         }
         __syncthreads();
@@ -224,22 +236,331 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
     __syncthreads();
-    // ---- shift: keep ring rows [y0+G-R, next_u) at the front ----
-    const int keep_lo = y0 + G - R;
-    const int drop = keep_lo - ring_lo;  // == G
-    const int keep = next_u - keep_lo;   // == 2R (<= RING - G)
-    for (int band = 0; band < keep; band += drop) {
-      const int nrow = min(drop, keep - band);
-      for (int j = warp; j < 2 * nrow; j += kNW) {
-        const int c = j / nrow, rr = band + j % nrow;
-        for (int i = lane; i < OX; i += 32)
-          ring[c * RING * RP + rr * RP + i] = ring[c * RING * RP + (rr + drop) * RP + i];
+    // ---- shift: keep ring rows [y0+G-R, y0+G+R) at the front (drop G rows) ----
+    // bands of G rows so that source and destination never overlap within a band
+#pragma unroll
+    for (int band = 0; band < 2 * R; band += G) {
+      const int nrow = (2 * R - band) < G ? (2 * R - band) : G;  // compile-time per band
+      for (int rr = band + warp; rr < band + nrow; rr += kNW)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          for (int i = lane; i < OX; i += 32)
+            ring[c * RING * RP + rr * RP + i] = ring[c * RING * RP + (rr + G) * RP + i];
+      __syncthreads();
+    }
+    ring_lo = y0 + G - R;
+  }
+  if (a.guard) flush_flags(flags, a.guard + (long long)b * a.guard_stride);
+}
+
+}  // namespace mr
+
+namespace mr {
+
+// ---------------------------------------------------------------------------------
+// Streaming adjoint of the velocity (objective.py:157-161, 165-169):
+//   mbar = -K^T vbar (kernel.py:48-68: zero-padded correlation + cumulative-weight
+//   edge taps at index 0 and n-1); zb += mbar . grad I; ib += G^T(mbar z).
+// Strip of OX computed columns (owners OX-2, one column of halo each side for
+// G^T); blocks of G computed rows (owners G-2).  vbar rows are TMA-staged
+// (zero fill outside the image = the transpose's zero padding), copied to an
+// odd pitch, filtered horizontally into the ring, then filtered vertically.
+// The epilogue operands (I, z, ib|v0, zb) of the block arrive by TMA while the
+// passes run.
+// ---------------------------------------------------------------------------------
+template <typename T, int R>
+struct StreamAdjCfg {
+  static constexpr int OX = 64;  // computed columns (owners OX-2)
+  static constexpr int G = 32;   // computed rows per block (owners G-2)
+  static constexpr int ADV = G - 2;
+  static constexpr int A = 16 / (int)sizeof(T);
+  static constexpr int RX = OX + 2 * R;
+  static constexpr int PXZ = round_up(RX + A - 1, A);  // vbar box width
+  static constexpr int PP = (RX % 2) ? RX : RX + 1;
+  static constexpr int RING = G + 2 * R;
+  static constexpr int RP = OX + 1;
+  static constexpr int OXP = OX + A;                   // epilogue box width
+  static constexpr int EPL = round_up(G * OXP, 32);    // one epilogue operand (I or z)
+  static constexpr int o_st = 0;  // vbar staging [2][G][PXZ]; after a block's last group: I, z
+  static constexpr int n_st1 = round_up(G * PXZ + A, 32);
+  static constexpr int o_p = o_st + 2 * n_st1;         // P [2][G][PP]; later res [2][G][RP]
+  static constexpr int n_p = round_up(2 * G * PP, 32);
+  static constexpr int o_ring = o_p + n_p;
+  static constexpr int n_ring = round_up(2 * RING * RP, 32);
+  static constexpr size_t head = 128;
+  static constexpr size_t bytes_reg = head + sizeof(T) * (size_t)(o_ring + n_ring);
+  static constexpr size_t bytes_noreg = bytes_reg;
+  static_assert(2 * G * RP <= n_p, "result must fit in the product buffer");
+  static_assert(2 * EPL <= 2 * n_st1, "epilogue I/z must fit in the staging buffer");
+};
+
+constexpr int kAdjStreamThreads = 256;
+
+template <typename T, int R, bool REG>
+__global__ void __launch_bounds__(kAdjStreamThreads)
+    k_velocity_adj2d_stream(VelAdjArgs<T> a, Taps<T> tp, const __grid_constant__ VelAdjMaps maps) {
+  using C = StreamAdjCfg<T, R>;
+  constexpr int NW = kAdjStreamThreads / 32;
+  constexpr int OX = C::OX, G = C::G, ADV = C::ADV, RX = C::RX, PXZ = C::PXZ, PP = C::PP,
+                RING = C::RING, RP = C::RP, OXP = C::OXP, EPL = C::EPL;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [0]: vbar groups, [1]: epilogue
+  T* base = reinterpret_cast<T*>(smem_raw + C::head);
+  T* st0 = base + C::o_st;
+  T* P = base + C::o_p;
+  T* ring = base + C::o_ring;
+  T* epi0 = base + C::o_st;  // epilogue I, z reuse the staging buffer
+
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.y;
+  const int x_org = blockIdx.x * (OX - 2) - 1;  // computed column 0
+  const int xs = x_org - R;                     // first input column
+  const int offV = align_shift(xs, C::A), offE = align_shift(x_org, C::A);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  unsigned ph0 = 0, ph1 = 0;
+  auto issue_v = [&](int u0) {
+    mbar_expect_tx(bar, (unsigned)(sizeof(T) * 2 * PXZ * G));
+    tma_load_3d(st0, &maps.vbar, xs - offV, u0, 2 * b, bar);
+    tma_load_3d(st0 + C::n_st1, &maps.vbar, xs - offV, u0, 2 * b + 1, bar);
+  };
+  auto issue_e = [&](int yc0) {
+    mbar_expect_tx(bar + 1, (unsigned)(sizeof(T) * OXP * G * 2));
+    const int xa = x_org - offE;
+    tma_load_3d(epi0, &maps.I, xa, yc0, b, bar + 1);
+    tma_load_3d(epi0 + EPL, &maps.z, xa, yc0, b, bar + 1);
+  };
+  if (tid == 0) issue_v(0);
+
+  unsigned bad = 0;
+  int ring_lo = -1 - R;  // image row of ring row 0
+  int next_u = -1 - R;   // next image row to produce (outside the image: zero rows)
+  for (int yb = 0; yb < H; yb += ADV) {
+    const int yc0 = yb - 1;  // computed row 0 of this block
+    const int need_hi = yc0 + G + R;
+    while (next_u < need_hi) {
+      const int u0 = next_u;
+      if (u0 < 0 || u0 >= H) {  // zero rows up to the image edge or to need_hi
+        const int cnt = u0 < 0 ? min(-u0, need_hi - u0) : need_hi - u0;
+        for (int j = warp; j < 2 * cnt; j += NW) {
+          const int c = j / cnt, rr = u0 + j % cnt;
+          for (int i = lane; i < OX; i += 32) ring[c * RING * RP + (rr - ring_lo) * RP + i] = T(0);
+        }
+        next_u = u0 + cnt;
+        continue;
       }
+      const int cnt = min(G, need_hi - u0);
+      const int cin = min(cnt, H - u0);
+      mbar_wait(bar, ph0);
+      ph0 ^= 1u;
+      // vbar rows -> odd-pitch P (zeros outside the image came from the TMA fill)
+      for (int r = warp; r < cin; r += NW)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const T* srow = st0 + c * C::n_st1 + offV + r * PXZ;
+          T* prow = P + c * G * PP + r * PP;
+          for (int i = lane; i < RX; i += 32) prow[i] = srow[i];
+        }
+      __syncthreads();
+      const int nu = u0 + cnt;
+      if (tid == 0 && nu < H && nu < need_hi) {  // next group of this block
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue_v(nu);
+      }
+      // horizontal transposed FIR of the new rows -> ring (lanes <-> rows)
+      constexpr int NB = OX / kRB;
+      for (int cb = warp; cb < 2 * NB; cb += NW) {
+        const int r = lane;
+        if (r >= cin) continue;
+        const int ib = cb % NB, c = cb / NB;
+        const T* src = P + c * G * PP + r * PP + ib * kRB;
+        T acc[kRB];
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+        for (int t = 0; t < kRB + 2 * R; ++t) {
+          const T x = src[t];
+#pragma unroll
+          for (int o = 0; o < kRB; ++o) {
+            const int tap = t - o;
+            if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+          }
+        }
+        const int gx0 = x_org + ib * kRB;
+        if (gx0 <= 0 && gx0 + kRB > 0) {  // column 0: sum_{d=0..R} W[R-d] g[d]
+          const int o = -gx0;
+          T s = T(0);
+#pragma unroll
+          for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[o + R + d], s);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+        }
+        if (gx0 <= W - 1 && gx0 + kRB > W - 1) {  // column n-1
+          const int o = W - 1 - gx0;
+          T s = T(0);
+#pragma unroll
+          for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[o + R + d], s);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+        }
+        T* dst = ring + c * RING * RP + (u0 + r - ring_lo) * RP + ib * kRB;
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
+      }
+      __syncthreads();
+      next_u = u0 + cin;
+    }
+    __syncthreads();
+    // staging is free: fetch the epilogue's I and z tiles while the vertical pass runs
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue_e(yc0);
+    }
+
+    // ---- owner operands of the epilogue into registers (in flight during the pass) ----
+    constexpr int NJ = (G - 2 + NW - 1) / NW, NI = (OX - 2 + 31) / 32;
+    T pre_a[NJ][NI], pre_b[NJ][NI], pre_c[NJ][NI];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < NI; ++ii) {
+        const int j = 1 + warp + jj * NW, i = 1 + lane + ii * 32;
+        const int gy = yc0 + j, gx = x_org + i;
+        const bool ok = j < G - 1 && i < OX - 1 && gy < H && gx < W;
+        const long long q = ok ? (long long)gy * W + gx : 0;
+        pre_a[jj][ii] = ok ? a.zb[b * N + q] : T(0);
+        if (REG) {
+          const T* __restrict__ w0 = a.v0 + b * 2 * N;
+          pre_b[jj][ii] = ok ? w0[q] : T(0);
+          pre_c[jj][ii] = ok ? w0[N + q] : T(0);
+        } else {
+          pre_b[jj][ii] = ok ? a.ib[b * N + q] : T(0);
+          pre_c[jj][ii] = T(0);
+        }
+      }
+
+    // ---- vertical transposed FIR for computed rows [yc0, yc0+G) -> res (= P) ----
+    T* res = P;  // [2][G][RP], holds mbar = -K^T vbar
+    constexpr int NBV = G / kRB;
+    constexpr int ICH = OX / 32;
+    for (int cb = warp; cb < 2 * NBV * ICH; cb += NW) {
+      const int ich = cb % ICH, jb = (cb / ICH) % NBV, c = cb / (ICH * NBV);
+      {
+        const int i = ich * 32 + lane;
+        const T* src = ring + c * RING * RP + (yc0 + jb * kRB - R - ring_lo) * RP + i;
+        T acc[kRB];
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+        for (int t = 0; t < kRB + 2 * R; ++t) {
+          const T x = src[t * RP];
+#pragma unroll
+          for (int o = 0; o < kRB; ++o) {
+            const int tap = t - o;
+            if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+          }
+        }
+        const int gy0 = yc0 + jb * kRB;
+        if (gy0 <= 0 && gy0 + kRB > 0) {
+          const int o = -gy0;
+          T s = T(0);
+#pragma unroll
+          for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[(o + R + d) * RP], s);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+        }
+        if (gy0 <= H - 1 && gy0 + kRB > H - 1) {
+          const int o = H - 1 - gy0;
+          T s = T(0);
+#pragma unroll
+          for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[(o + R + d) * RP], s);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+        }
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) res[c * G * RP + (jb * kRB + o) * RP + i] = -acc[o];
+      }
+    }
+    mbar_wait(bar + 1, ph1);
+    ph1 ^= 1u;
+    __syncthreads();
+
+    // ---- epilogue on owners: rows j in [1, G-1), cols i in [1, OX-1) ----
+    const T* tI = epi0 + offE;
+    const T* tz = tI + EPL;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+    for (int ii = 0; ii < NI; ++ii) {
+      const int j = 1 + warp + jj * NW, i = 1 + lane + ii * 32;
+      const int gy = yc0 + j, gx = x_org + i;
+      if (j >= G - 1 || i >= OX - 1 || gy >= H || gx >= W) continue;
+      {
+        const long long q = (long long)gy * W + gx;
+        const int e = j * OXP + i;
+        const T cI = tI[e];
+        const T g0 = grad1(tI[e - OXP], cI, tI[e + OXP], gy, H);
+        const T g1 = grad1(tI[e - 1], cI, tI[e + 1], gx, W);
+        const T m0 = res[j * RP + i];
+        const T m1 = res[G * RP + j * RP + i];
+        T zb_new = pre_a[jj][ii] + (m0 * g0 + m1 * g1);  // objective.py:159
+        if (REG) {
+          const T km = -(pre_b[jj][ii] * g0 + pre_c[jj][ii] * g1);
+          zb_new = zb_new + a.lam * (km + a.two_rho * tz[e]);
+          a.zout[b * N + q] = zb_new;
+          bad |= isfinite(zb_new) ? 0u : 1u;
+        } else {
+          a.zb[b * N + q] = zb_new;
+          auto q0 = [&](int jr) { return res[jr * RP + i] * tz[jr * OXP + i]; };
+          auto q1 = [&](int ic) { return res[G * RP + j * RP + ic] * tz[j * OXP + ic]; };
+          const T zc = tz[e];
+          const T qc0 = m0 * zc, qc1 = m1 * zc;
+          const T gm = (gy > 0) ? q0(j - 1) : T(0);
+          const T gp = (gy < H - 1) ? q0(j + 1) : T(0);
+          const T gf = (gy == 0) ? qc0 : ((gy == 1) ? gm : T(0));
+          const T gl = (gy == H - 1) ? qc0 : ((gy == H - 2) ? gp : T(0));
+          const T t0 = diff_adj1(gm, gp, gf, gl, gy, H);
+          const T hm = (gx > 0) ? q1(i - 1) : T(0);
+          const T hp = (gx < W - 1) ? q1(i + 1) : T(0);
+          const T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
+          const T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
+          const T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
+          a.ib[b * N + q] = pre_b[jj][ii] + (t0 + t1);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- shift the ring by ADV rows ----
+    const int keep_lo = yc0 + ADV - R;  // first row needed by the next block
+    constexpr int drop = ADV;           // == keep_lo - ring_lo
+    constexpr int keep = G + 2 * R - ADV;  // == next_u - keep_lo
+#pragma unroll
+    for (int band = 0; band < keep; band += drop) {
+      const int nrow = (keep - band) < drop ? (keep - band) : drop;
+      for (int rr = band + warp; rr < band + nrow; rr += NW)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          for (int i = lane; i < OX; i += 32)
+            ring[c * RING * RP + rr * RP + i] = ring[c * RING * RP + (rr + drop) * RP + i];
       __syncthreads();
     }
     ring_lo = keep_lo;
+    if (tid == 0 && next_u < H) {  // the next block's first group
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue_v(next_u);
+    }
   }
-  if (a.guard) flush_flags(flags, a.guard + (long long)b * a.guard_stride);
+  if (REG) {
+    unsigned all = __reduce_or_sync(0xffffffffu, bad);
+    if (all && lane == 0) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+  }
 }
 
 }  // namespace mr
