@@ -509,6 +509,36 @@ struct AdjArgs {
 
 constexpr int kAdjTX = 32, kAdjTY = kThreads / 32;
 
+// Scatter of the four bilinear-transpose contributions of one pixel
+// (bilinear_adjoint_values, fields.py:243-254) with warp-level merging: lanes
+// are consecutive x of one row, so where lane l-1's right cells are lane l's
+// left cells (same integer offset) lane l adds them and lane l-1 skips its
+// own -> ~2 instead of 4 red.global.add per pixel on smooth fields.
+template <typename T>
+__device__ __forceinline__ void scatter4_merged(T* __restrict__ out, long long cell, bool valid,
+                                                long long W, T ca, T cb, T cc, T cd) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long key = valid ? cell : -4;
+  const long long prev_key = __shfl_up_sync(full, key, 1);
+  const long long next_key = __shfl_down_sync(full, key, 1);
+  const T pc = __shfl_up_sync(full, cc, 1);
+  const T pd = __shfl_up_sync(full, cd, 1);
+  if (!valid) return;
+  const bool merge_left = lane > 0 && prev_key >= 0 && prev_key + 1 == key;
+  const bool merged_by_next = lane < 31 && next_key >= 0 && key + 1 == next_key;
+  if (merge_left) {
+    ca += pc;
+    cb += pd;
+  }
+  atomicAdd(out + cell, ca);
+  atomicAdd(out + cell + W, cb);
+  if (!merged_by_next) {
+    atomicAdd(out + cell + 1, cc);
+    atomicAdd(out + cell + W + 1, cd);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   __shared__ T s_div[kAdjTY + 2][kAdjTX + 2];  // s = -dt * zbar * B(z), halo 1
@@ -523,88 +553,90 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   const T* __restrict__ ibar = a.ibar + b * N;
   const T* __restrict__ zbar = a.zbar + b * N;
   const T dt = a.dt;
-
-  // s on the tile + 1 halo (needed by the divergence adjoint, objective.py:145-147)
-  for (int p = threadIdx.x; p < (kAdjTY + 2) * (kAdjTX + 2); p += kThreads) {
-    int j = p / (kAdjTX + 2), i = p - j * (kAdjTX + 2);
-    int gy = y0 - 1 + j, gx = x0 - 1 + i;
-    T s = T(0);
-    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-      long long q = (long long)gy * W + gx;
-      AxisPlan<T> py = plan_axis<T>(gy, v0[q], dt, H);
-      AxisPlan<T> px = plan_axis<T>(gx, v1[q], dt, W);
-      long long c00 = (long long)py.i0 * W + px.i0;
-      T bz = bilerp(z[c00], z[c00 + W], z[c00 + 1], z[c00 + W + 1], py.f, px.f);
-      s = -dt * (zbar[q] * bz);
-    }
-    s_div[j][i] = s;
-  }
-  __syncthreads();
-
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x = x0 + tx, y = y0 + ty;
-  if (x >= W || y >= H) return;
-  const long long q = (long long)y * W + x;
-  const T vy = v0[q], vx = v1[q];
-  const AxisPlan<T> py = plan_axis<T>(y, vy, dt, H);
-  const AxisPlan<T> px = plan_axis<T>(x, vx, dt, W);
+  const bool own = x < W && y < H;
+  const long long q = own ? (long long)y * W + x : 0;
+
+  // ---- owner pixel: plan, corners, adjoint values (objective.py:128-147) ----
+  const T vy = own ? v0[q] : T(0), vx = own ? v1[q] : T(0);
+  const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
+  const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
   const long long c00 = (long long)py.i0 * W + px.i0;
   const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
   const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
-  const T ib_ = ibar[q];
-  const T zb_ = zbar[q];
-
-  // image update: ib = P^T ibar; vbar = -dt * dB(I)/dcoord * ibar (objective.py:128-132)
-  T* __restrict__ ibo = a.ib + b * N;
-  T* __restrict__ zbo = a.zb + b * N;
-  atomicAdd(ibo + c00, wy * wx * ib_);
-  atomicAdd(ibo + c10, fy * wx * ib_);
-  atomicAdd(ibo + c01, wy * fx * ib_);
-  atomicAdd(ibo + c11, fy * fx * ib_);
-  {
-    T ia = I[c00], ib2 = I[c10], ic = I[c01], id = I[c11];
-    T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
-    T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
-    T vb0 = -dt * ddy * ib_;
-    T vb1 = -dt * ddx * ib_;
-    // momentum update (objective.py:136-147)
+  const T ib_ = own ? ibar[q] : T(0);
+  const T zb_ = own ? zbar[q] : T(0);
+  const T za = z[c00], zb2 = z[c10], zc = z[c01], zd = z[c11];
+  const T ia = I[c00], ib2 = I[c10], ic = I[c01], id = I[c11];
+  T scale = T(1);
+  if (own) {
     const T up = (y > 0) ? v0[q - W] : vy;
     const T dn = (y < H - 1) ? v0[q + W] : vy;
     const T lf = (x > 0) ? v1[q - 1] : vx;
     const T rt = (x < W - 1) ? v1[q + 1] : vx;
-    const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
-    const T scale = T(1) - dt * div;
-    const T wz = zb_ * scale;
-    if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);  // zb = dt*mu*ibar (:133)
-    atomicAdd(zbo + c00, wy * wx * wz);
-    atomicAdd(zbo + c10, fy * wx * wz);
-    atomicAdd(zbo + c01, wy * fx * wz);
-    atomicAdd(zbo + c11, fy * fx * wz);
-    T za = z[c00], zb2 = z[c10], zc = z[c01], zd = z[c11];
-    T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
-    T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
-    vb0 += -dt * dzy * wz;
-    vb1 += -dt * dzx * wz;
-    // divergence adjoint: vbar_c += D_c^T s (objective.py:145-147)
-    const int j = ty + 1, i = tx + 1;
-    const T sm_ = s_div[j - 1][i], sp_ = s_div[j + 1][i];
-    const T s_first_y = (y <= 1) ? s_div[j - y][i] : T(0);
-    const T s_last_y = (y >= H - 2) ? s_div[j + (H - 1 - y)][i] : T(0);
-    vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
-    const T sl_ = s_div[j][i - 1], sr_ = s_div[j][i + 1];
-    const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
-    const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
-    vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
-    if (a.reg_lam != T(0)) {
-      T g0, g1;
-      grad2(I, y, x, H, W, g0, g1);
-      const T zz = z[q];
-      vb0 = vb0 - a.reg_lam * (zz * g0);
-      vb1 = vb1 - a.reg_lam * (zz * g1);
-    }
-    a.vbar[b * 2 * N + q] = vb0;
-    a.vbar[b * 2 * N + N + q] = vb1;
+    scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
   }
+  s_div[ty + 1][tx + 1] = own ? -dt * (zb_ * bilerp(za, zb2, zc, zd, fy, fx)) : T(0);
+
+  // ---- s on the 1-pixel halo ring of the tile ----
+  constexpr int NHALO = 2 * (kAdjTX + 2) + 2 * kAdjTY;
+  for (int h = threadIdx.x; h < NHALO; h += kThreads) {
+    int j, i;
+    if (h < kAdjTX + 2) { j = 0; i = h; }
+    else if (h < 2 * (kAdjTX + 2)) { j = kAdjTY + 1; i = h - (kAdjTX + 2); }
+    else { const int k = h - 2 * (kAdjTX + 2); j = 1 + (k >> 1); i = (k & 1) ? kAdjTX + 1 : 0; }
+    const int gy = y0 - 1 + j, gx = x0 - 1 + i;
+    T sv = T(0);
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+      const long long qq = (long long)gy * W + gx;
+      const AxisPlan<T> hy = plan_axis<T>(gy, v0[qq], dt, H);
+      const AxisPlan<T> hx = plan_axis<T>(gx, v1[qq], dt, W);
+      const long long h00 = (long long)hy.i0 * W + hx.i0;
+      sv = -dt * (zbar[qq] * bilerp(z[h00], z[h00 + W], z[h00 + 1], z[h00 + W + 1], hy.f, hx.f));
+    }
+    s_div[j][i] = sv;
+  }
+
+  // ---- scatters: ib = P^T ibar; zb = P^T (zbar*scale) + dt mu ibar ----
+  T* __restrict__ ibo = a.ib + b * N;
+  T* __restrict__ zbo = a.zb + b * N;
+  const T wz = zb_ * scale;
+  scatter4_merged(ibo, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
+                  fy * fx * ib_);
+  scatter4_merged(zbo, c00, own, (long long)W, wy * wx * wz, fy * wx * wz, wy * fx * wz,
+                  fy * fx * wz);
+  if (own && a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);  // zb = dt*mu*ibar (:133)
+  __syncthreads();
+  if (!own) return;
+
+  // ---- vbar (objective.py:131-132, 143-147) ----
+  const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
+  const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
+  T vb0 = -dt * ddy * ib_;
+  T vb1 = -dt * ddx * ib_;
+  const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
+  const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
+  vb0 += -dt * dzy * wz;
+  vb1 += -dt * dzx * wz;
+  const int j = ty + 1, i = tx + 1;
+  const T sm_ = s_div[j - 1][i], sp_ = s_div[j + 1][i];
+  const T s_first_y = (y <= 1) ? s_div[j - y][i] : T(0);
+  const T s_last_y = (y >= H - 2) ? s_div[j + (H - 1 - y)][i] : T(0);
+  vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+  const T sl_ = s_div[j][i - 1], sr_ = s_div[j][i + 1];
+  const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
+  const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
+  vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+  if (a.reg_lam != T(0)) {
+    T g0, g1;
+    grad2(I, y, x, H, W, g0, g1);
+    const T zz = z[q];
+    vb0 = vb0 - a.reg_lam * (zz * g0);
+    vb1 = vb1 - a.reg_lam * (zz * g1);
+  }
+  a.vbar[b * 2 * N + q] = vb0;
+  a.vbar[b * 2 * N + N + q] = vb1;
 }
 
 // ------------------------------------------------------------------------------
