@@ -148,7 +148,7 @@ static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, co
   StepArgs<T> a{I,     z,       v,      In,        zn,          phi_in,
                 phi_out, (T)dt, (T)(dt * mu), mu != 0.0, guard_in, guard_out,
                 guard_stride, g};
-  dim3 grid((g.W + 31) / 32, (g.H + kThreads / 32 - 1) / (kThreads / 32), g.B);
+  dim3 grid((g.W + 31) / 32, (g.H + kStepRows - 1) / kStepRows, g.B);
   k_sl_step2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
 }

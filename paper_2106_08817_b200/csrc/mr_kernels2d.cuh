@@ -426,54 +426,99 @@ struct StepArgs {
   Grid2 g;
 };
 
+// Each thread handles kStepPix pixels of one column (rows kThreads/32 apart):
+// all loads of a phase are issued before any is consumed, so enough bytes are
+// in flight to cover HBM latency (the one-pixel form stalled on its v load).
+constexpr int kStepPix = 2;
+constexpr int kStepRows = (kThreads / 32) * kStepPix;  // rows per block
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_step2d(StepArgs<T> a) {
   const int H = a.g.H, W = a.g.W;
   const int x = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int y = blockIdx.y * (kThreads / 32) + (threadIdx.x >> 5);
+  const int yb = blockIdx.y * kStepRows + (threadIdx.x >> 5);
   const int b = blockIdx.z;
-  if (x >= W || y >= H) return;
+  if (x >= W) return;
   const long long N = a.g.N;
-  const long long q = (long long)y * W + x;
   const T* __restrict__ I = a.I + b * N;
   const T* __restrict__ z = a.z + b * N;
   const T* __restrict__ v0 = a.v + b * 2 * N;
   const T* __restrict__ v1 = v0 + N;
-  const T vy = v0[q], vx = v1[q];
-  const AxisPlan<T> py = plan_axis<T>(y, vy, a.dt, H);
-  const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
-  const long long c00 = (long long)py.i0 * W + px.i0;
-  const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
-  if (a.guard_in) {  // _guard(0, image, momentum) on the inputs (integrator.py:184)
-    const unsigned fin = guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE) |
-                         guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
-    if (fin) atomicOr(reinterpret_cast<int*>(a.guard_in + (long long)b * a.guard_stride), (int)fin);
-  }
-  T bi = bilerp(I[c00], I[c10], I[c01], I[c11], py.f, px.f);
-  if (a.has_mu) bi = bi + a.dtmu * z[q];  // advect_image_sl_arr: + dt*mu*z
-  const T bz = bilerp(z[c00], z[c10], z[c01], z[c11], py.f, px.f);
-  // divergence_arr (fields.py:169-170)
-  const T up = (y > 0) ? v0[q - W] : vy;
-  const T dn = (y < H - 1) ? v0[q + W] : vy;
-  const T lf = (x > 0) ? v1[q - 1] : vx;
-  const T rt = (x < W - 1) ? v1[q + 1] : vx;
-  const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
-  const T zn = bz * (T(1) - a.dt * div);
-  a.In[b * N + q] = bi;
-  a.zn[b * N + q] = zn;
-  if (a.guard_out) {  // flags are almost always zero: no warp reduction needed
-    const unsigned fout = guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) |
-                          guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
-    if (fout)
-      atomicOr(reinterpret_cast<int*>(a.guard_out + (long long)b * a.guard_stride), (int)fout);
-  }
-  if (a.phi_in) {
+  int yy[kStepPix];
+  bool act[kStepPix];
+  long long q[kStepPix];
+  T vy[kStepPix], vx[kStepPix], up[kStepPix], dn[kStepPix], lf[kStepPix], rt[kStepPix];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const T* __restrict__ ph = a.phi_in + (b * 2 + c) * N;
-      a.phi_out[(b * 2 + c) * N + q] = bilerp(ph[c00], ph[c10], ph[c01], ph[c11], py.f, px.f);
+  for (int k = 0; k < kStepPix; ++k) {
+    yy[k] = yb + k * (kThreads / 32);
+    act[k] = yy[k] < H;
+    const int y = act[k] ? yy[k] : H - 1;
+    q[k] = (long long)y * W + x;
+  }
+#pragma unroll
+  for (int k = 0; k < kStepPix; ++k) {
+    const int y = act[k] ? yy[k] : H - 1;
+    vy[k] = v0[q[k]];
+    vx[k] = v1[q[k]];
+    up[k] = v0[y > 0 ? q[k] - W : q[k]];
+    dn[k] = v0[y < H - 1 ? q[k] + W : q[k]];
+    lf[k] = v1[x > 0 ? q[k] - 1 : q[k]];
+    rt[k] = v1[x < W - 1 ? q[k] + 1 : q[k]];
+  }
+  AxisPlan<T> py[kStepPix], px[kStepPix];
+  long long c00[kStepPix];
+#pragma unroll
+  for (int k = 0; k < kStepPix; ++k) {
+    const int y = act[k] ? yy[k] : H - 1;
+    py[k] = plan_axis<T>(y, vy[k], a.dt, H);
+    px[k] = plan_axis<T>(x, vx[k], a.dt, W);
+    c00[k] = (long long)py[k].i0 * W + px[k].i0;
+  }
+  T ci[kStepPix][4], cz[kStepPix][4], zq[kStepPix];
+#pragma unroll
+  for (int k = 0; k < kStepPix; ++k) {
+    ci[k][0] = I[c00[k]];
+    ci[k][1] = I[c00[k] + W];
+    ci[k][2] = I[c00[k] + 1];
+    ci[k][3] = I[c00[k] + W + 1];
+    cz[k][0] = z[c00[k]];
+    cz[k][1] = z[c00[k] + W];
+    cz[k][2] = z[c00[k] + 1];
+    cz[k][3] = z[c00[k] + W + 1];
+    zq[k] = (a.has_mu || a.guard_in) ? z[q[k]] : T(0);
+  }
+  unsigned fin = 0, fout = 0;
+#pragma unroll
+  for (int k = 0; k < kStepPix; ++k) {
+    if (!act[k]) continue;
+    const int y = yy[k];
+    if (a.guard_in) {  // _guard(0, image, momentum) on the inputs (integrator.py:184)
+      fin |= guard_bits(I[q[k]], MR_GUARD_IMAGE_NONFINITE) |
+             guard_bits(zq[k], MR_GUARD_MOMENTUM_NONFINITE);
+    }
+    T bi = bilerp(ci[k][0], ci[k][1], ci[k][2], ci[k][3], py[k].f, px[k].f);
+    if (a.has_mu) bi = bi + a.dtmu * zq[k];  // advect_image_sl_arr: + dt*mu*z
+    const T bz = bilerp(cz[k][0], cz[k][1], cz[k][2], cz[k][3], py[k].f, px[k].f);
+    // divergence_arr (fields.py:169-170)
+    const T div = grad1(up[k], vy[k], dn[k], y, H) + grad1(lf[k], vx[k], rt[k], x, W);
+    const T zn = bz * (T(1) - a.dt * div);
+    a.In[b * N + q[k]] = bi;
+    a.zn[b * N + q[k]] = zn;
+    fout |= guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) | guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+    if (a.phi_in) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const T* __restrict__ ph = a.phi_in + (b * 2 + c) * N;
+        a.phi_out[(b * 2 + c) * N + q[k]] = bilerp(ph[c00[k]], ph[c00[k] + W], ph[c00[k] + 1],
+                                                   ph[c00[k] + W + 1], py[k].f, px[k].f);
+      }
     }
   }
+  // flags are almost always zero: no warp reduction needed
+  if (fin && a.guard_in)
+    atomicOr(reinterpret_cast<int*>(a.guard_in + (long long)b * a.guard_stride), (int)fin);
+  if (fout && a.guard_out)
+    atomicOr(reinterpret_cast<int*>(a.guard_out + (long long)b * a.guard_stride), (int)fout);
 }
 
 template <typename T>
