@@ -158,7 +158,7 @@ static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I,
                                const T* v, const T* ibar, const T* zbar, T* ib, T* zb, T* vbar,
                                cudaStream_t s, double reg_lam = 0.0) {
   AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, (T)reg_lam, g};
-  dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjTY - 1) / kAdjTY, g.B);
+  dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjRows - 1) / kAdjRows, g.B);
   k_sl_adjoint2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
 }

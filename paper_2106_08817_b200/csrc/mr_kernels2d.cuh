@@ -584,13 +584,16 @@ __device__ __forceinline__ void scatter4_merged(T* __restrict__ out, long long c
   }
 }
 
+constexpr int kAdjPix = 1;                       // pixels per thread (rows kAdjTY apart)
+constexpr int kAdjRows = kAdjTY * kAdjPix;        // tile rows
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
-  __shared__ T s_div[kAdjTY + 2][kAdjTX + 2];  // s = -dt * zbar * B(z), halo 1
+  __shared__ T s_div[kAdjRows + 2][kAdjTX + 2];  // s = -dt * zbar * B(z), halo 1
   const int H = a.g.H, W = a.g.W;
   const long long N = a.g.N;
   const int b = blockIdx.z;
-  const int x0 = blockIdx.x * kAdjTX, y0 = blockIdx.y * kAdjTY;
+  const int x0 = blockIdx.x * kAdjTX, y0 = blockIdx.y * kAdjRows;
   const T* __restrict__ I = a.I + b * N;
   const T* __restrict__ z = a.z + b * N;
   const T* __restrict__ v0 = a.v + b * 2 * N;
@@ -599,37 +602,67 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   const T* __restrict__ zbar = a.zbar + b * N;
   const T dt = a.dt;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int x = x0 + tx, y = y0 + ty;
-  const bool own = x < W && y < H;
-  const long long q = own ? (long long)y * W + x : 0;
+  const int x = x0 + tx;
 
-  // ---- owner pixel: plan, corners, adjoint values (objective.py:128-147) ----
-  const T vy = own ? v0[q] : T(0), vx = own ? v1[q] : T(0);
-  const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
-  const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
-  const long long c00 = (long long)py.i0 * W + px.i0;
-  const long long c10 = c00 + W, c01 = c00 + 1, c11 = c10 + 1;
-  const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
-  const T ib_ = own ? ibar[q] : T(0);
-  const T zb_ = own ? zbar[q] : T(0);
-  const T za = z[c00], zb2 = z[c10], zc = z[c01], zd = z[c11];
-  const T ia = I[c00], ib2 = I[c10], ic = I[c01], id = I[c11];
-  T scale = T(1);
-  if (own) {
-    const T up = (y > 0) ? v0[q - W] : vy;
-    const T dn = (y < H - 1) ? v0[q + W] : vy;
-    const T lf = (x > 0) ? v1[q - 1] : vx;
-    const T rt = (x < W - 1) ? v1[q + 1] : vx;
-    scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
+  int yy[kAdjPix];
+  bool own[kAdjPix];
+  long long q[kAdjPix];
+  T vy[kAdjPix], vx[kAdjPix], up[kAdjPix], dn[kAdjPix], lf[kAdjPix], rt[kAdjPix];
+  T ibv[kAdjPix], zbv[kAdjPix];
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    yy[k] = y0 + ty + k * kAdjTY;
+    own[k] = x < W && yy[k] < H;
+    const int y = own[k] ? yy[k] : 0;
+    const int xc = own[k] ? x : 0;
+    q[k] = (long long)y * W + xc;
+    vy[k] = v0[q[k]];
+    vx[k] = v1[q[k]];
+    up[k] = v0[y > 0 ? q[k] - W : q[k]];
+    dn[k] = v0[y < H - 1 ? q[k] + W : q[k]];
+    lf[k] = v1[xc > 0 ? q[k] - 1 : q[k]];
+    rt[k] = v1[xc < W - 1 ? q[k] + 1 : q[k]];
+    ibv[k] = ibar[q[k]];
+    zbv[k] = zbar[q[k]];
   }
-  s_div[ty + 1][tx + 1] = own ? -dt * (zb_ * bilerp(za, zb2, zc, zd, fy, fx)) : T(0);
+  AxisPlan<T> py[kAdjPix], px[kAdjPix];
+  long long c00[kAdjPix];
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    py[k] = plan_axis<T>(own[k] ? yy[k] : 0, vy[k], dt, H);
+    px[k] = plan_axis<T>(own[k] ? x : 0, vx[k], dt, W);
+    c00[k] = (long long)py[k].i0 * W + px[k].i0;
+  }
+  T ci[kAdjPix][4], cz[kAdjPix][4];
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    ci[k][0] = I[c00[k]];
+    ci[k][1] = I[c00[k] + W];
+    ci[k][2] = I[c00[k] + 1];
+    ci[k][3] = I[c00[k] + W + 1];
+    cz[k][0] = z[c00[k]];
+    cz[k][1] = z[c00[k] + W];
+    cz[k][2] = z[c00[k] + 1];
+    cz[k][3] = z[c00[k] + W + 1];
+  }
+  T wz[kAdjPix];
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    const int y = own[k] ? yy[k] : 0;
+    const T scale = T(1) - dt * (grad1(up[k], vy[k], dn[k], y, H) +
+                                 grad1(lf[k], vx[k], rt[k], own[k] ? x : 0, W));
+    wz[k] = zbv[k] * scale;
+    s_div[ty + k * kAdjTY + 1][tx + 1] =
+        own[k] ? -dt * (zbv[k] * bilerp(cz[k][0], cz[k][1], cz[k][2], cz[k][3], py[k].f, px[k].f))
+               : T(0);
+  }
 
   // ---- s on the 1-pixel halo ring of the tile ----
-  constexpr int NHALO = 2 * (kAdjTX + 2) + 2 * kAdjTY;
+  constexpr int NHALO = 2 * (kAdjTX + 2) + 2 * kAdjRows;
   for (int h = threadIdx.x; h < NHALO; h += kThreads) {
     int j, i;
     if (h < kAdjTX + 2) { j = 0; i = h; }
-    else if (h < 2 * (kAdjTX + 2)) { j = kAdjTY + 1; i = h - (kAdjTX + 2); }
+    else if (h < 2 * (kAdjTX + 2)) { j = kAdjRows + 1; i = h - (kAdjTX + 2); }
     else { const int k = h - 2 * (kAdjTX + 2); j = 1 + (k >> 1); i = (k & 1) ? kAdjTX + 1 : 0; }
     const int gy = y0 - 1 + j, gx = x0 - 1 + i;
     T sv = T(0);
@@ -646,42 +679,53 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   // ---- scatters: ib = P^T ibar; zb = P^T (zbar*scale) + dt mu ibar ----
   T* __restrict__ ibo = a.ib + b * N;
   T* __restrict__ zbo = a.zb + b * N;
-  const T wz = zb_ * scale;
-  scatter4_merged(ibo, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
-                  fy * fx * ib_);
-  scatter4_merged(zbo, c00, own, (long long)W, wy * wx * wz, fy * wx * wz, wy * fx * wz,
-                  fy * fx * wz);
-  if (own && a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);  // zb = dt*mu*ibar (:133)
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    const T fy = py[k].f, fx = px[k].f, wy = T(1) - fy, wx = T(1) - fx;
+    const T g = ibv[k], w = wz[k];
+    scatter4_merged(ibo, c00[k], own[k], (long long)W, wy * wx * g, fy * wx * g, wy * fx * g,
+                    fy * fx * g);
+    scatter4_merged(zbo, c00[k], own[k], (long long)W, wy * wx * w, fy * wx * w, wy * fx * w,
+                    fy * fx * w);
+    if (own[k] && a.has_mu) atomicAdd(zbo + q[k], a.dtmu * g);  // zb = dt*mu*ibar (:133)
+  }
   __syncthreads();
-  if (!own) return;
 
   // ---- vbar (objective.py:131-132, 143-147) ----
-  const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
-  const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
-  T vb0 = -dt * ddy * ib_;
-  T vb1 = -dt * ddx * ib_;
-  const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
-  const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
-  vb0 += -dt * dzy * wz;
-  vb1 += -dt * dzx * wz;
-  const int j = ty + 1, i = tx + 1;
-  const T sm_ = s_div[j - 1][i], sp_ = s_div[j + 1][i];
-  const T s_first_y = (y <= 1) ? s_div[j - y][i] : T(0);
-  const T s_last_y = (y >= H - 2) ? s_div[j + (H - 1 - y)][i] : T(0);
-  vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
-  const T sl_ = s_div[j][i - 1], sr_ = s_div[j][i + 1];
-  const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
-  const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
-  vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
-  if (a.reg_lam != T(0)) {
-    T g0, g1;
-    grad2(I, y, x, H, W, g0, g1);
-    const T zz = z[q];
-    vb0 = vb0 - a.reg_lam * (zz * g0);
-    vb1 = vb1 - a.reg_lam * (zz * g1);
+#pragma unroll
+  for (int k = 0; k < kAdjPix; ++k) {
+    if (!own[k]) continue;
+    const int y = yy[k];
+    const T fy = py[k].f, fx = px[k].f, wy = T(1) - fy, wx = T(1) - fx;
+    const T ia = ci[k][0], ib2 = ci[k][1], ic = ci[k][2], id = ci[k][3];
+    const T za = cz[k][0], zb2 = cz[k][1], zc = cz[k][2], zd = cz[k][3];
+    const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py[k].inside ? T(1) : T(0));
+    const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px[k].inside ? T(1) : T(0));
+    T vb0 = -dt * ddy * ibv[k];
+    T vb1 = -dt * ddx * ibv[k];
+    const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py[k].inside ? T(1) : T(0));
+    const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px[k].inside ? T(1) : T(0));
+    vb0 += -dt * dzy * wz[k];
+    vb1 += -dt * dzx * wz[k];
+    const int j = ty + k * kAdjTY + 1, i = tx + 1;
+    const T sm_ = s_div[j - 1][i], sp_ = s_div[j + 1][i];
+    const T s_first_y = (y <= 1) ? s_div[j - y][i] : T(0);
+    const T s_last_y = (y >= H - 2) ? s_div[j + (H - 1 - y)][i] : T(0);
+    vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+    const T sl_ = s_div[j][i - 1], sr_ = s_div[j][i + 1];
+    const T s_first_x = (x <= 1) ? s_div[j][i - x] : T(0);
+    const T s_last_x = (x >= W - 2) ? s_div[j][i + (W - 1 - x)] : T(0);
+    vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    if (a.reg_lam != T(0)) {
+      T g0, g1;
+      grad2(I, y, x, H, W, g0, g1);
+      const T zz = z[q[k]];
+      vb0 = vb0 - a.reg_lam * (zz * g0);
+      vb1 = vb1 - a.reg_lam * (zz * g1);
+    }
+    a.vbar[b * 2 * N + q[k]] = vb0;
+    a.vbar[b * 2 * N + N + q[k]] = vb1;
   }
-  a.vbar[b * 2 * N + q] = vb0;
-  a.vbar[b * 2 * N + N + q] = vb1;
 }
 
 // ------------------------------------------------------------------------------
