@@ -149,6 +149,16 @@ __device__ __forceinline__ void cp_async_elem_zfill(T* smem, const T* gmem, bool
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// ---- packed FP32x2 FMA (FFMA2, sm_100a): two FMAs per issue slot ----------------
+__device__ __forceinline__ float2 ffma2(float2 a, float w, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %4};\n"
+      "mov.b64 rc, {%5, %6};\nfma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(w), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // ---- TMA (cp.async.bulk.tensor) + mbarrier ---------------------------------------
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

@@ -77,6 +77,64 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
   const int lane = tid & 31, warp = tid >> 5;
   // ---- pass 1: along axis 0 (rows), for every region column ----
   constexpr int NB1 = OY / kRB;
+  if constexpr (sizeof(T) == 4) {
+    // fp32: two adjacent columns per thread, packed FFMA2 on (col i, col i+1) with
+    // 8-byte aligned smem pairs (the pair grid follows the smem address parity)
+    const int par = (int)((reinterpret_cast<uintptr_t>(rg) >> 2) & 1);
+    const int npairs = (RX + par + 1) / 2;
+    for (int cb = warp; cb < C * NB1; cb += kNW)
+    for (int pp = lane; pp < npairs; pp += 32) {
+      const int jb = cb % NB1;
+      const int c = cb / NB1;
+      const int i0 = 2 * pp - par;
+      const float2* src = reinterpret_cast<const float2*>(rg + c * CS + jb * kRB * PX + i0);
+      float2 acc[kRB];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const float2 x = src[t * (PX / 2)];
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
+        }
+      }
+      if (TRANSPOSE) {
+        const int gy0 = y_org + jb * kRB;
+        const float* fsrc = reinterpret_cast<const float*>(src);
+        if (gy0 <= 0 && gy0 + kRB > 0) {
+          const int o = -gy0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = 0; d <= R; ++d)
+            s2 = ffma2(make_float2(fsrc[(o + R + d) * PX], fsrc[(o + R + d) * PX + 1]),
+                       (float)tp.e[R - d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+        if (gy0 <= H - 1 && gy0 + kRB > H - 1) {
+          const int o = H - 1 - gy0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = -R; d <= 0; ++d)
+            s2 = ffma2(make_float2(fsrc[(o + R + d) * PX], fsrc[(o + R + d) * PX + 1]),
+                       (float)tp.e[R + d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+      }
+      T* dst = vt + (c * OY + jb * kRB) * VP + i0;
+      if (i0 >= 0 && i0 < RX) {
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) dst[o * VP] = acc[o].x;
+      }
+      if (i0 + 1 < RX) {
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) dst[o * VP + 1] = acc[o].y;
+      }
+    }
+  } else {
   for (int cb = warp; cb < C * NB1; cb += kNW)
   for (int i = lane; i < RX; i += 32) {
     const int jb = cb % NB1;
@@ -116,6 +174,7 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
     T* dst = vt + (c * OY + jb * kRB) * VP + i;
 #pragma unroll
     for (int o = 0; o < kRB; ++o) dst[o * VP] = acc[o];
+  }
   }
   __syncthreads();
   mid();
