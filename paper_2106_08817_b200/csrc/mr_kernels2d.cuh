@@ -183,6 +183,57 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
   constexpr int NB2 = OX / kRB;
   T* res = rg;
   static_assert(OY == 32, "pass 2 maps lanes to the 32 rows of a tile");
+  if constexpr (sizeof(T) == 4) {
+    // fp32: rows (j, j+16) packed per thread (FFMA2); half-warps take two column blocks
+    static_assert(NB2 % 2 == 0, "column blocks come in pairs");
+    for (int cb = warp; cb < C * NB2 / 2; cb += kNW) {
+      const int j = lane & 15;
+      const int ib = 2 * (cb % (NB2 / 2)) + (lane >> 4);
+      const int c = cb / (NB2 / 2);
+      const T* s0 = vt + (c * OY + j) * VP + ib * kRB;
+      const T* s1 = s0 + 16 * VP;
+      float2 acc[kRB];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const float2 x = make_float2(s0[t], s1[t]);
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
+        }
+      }
+      if (TRANSPOSE) {
+        const int gx0 = x_org + ib * kRB;
+        if (gx0 <= 0 && gx0 + kRB > 0) {
+          const int o = -gx0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = 0; d <= R; ++d)
+            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R - d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+        if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
+          const int o = W - 1 - gx0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = -R; d <= 0; ++d)
+            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R + d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+      }
+      T* d0 = res + (c * OY + j) * OP + ib * kRB;
+      T* d1 = d0 + 16 * OP;
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        d0[o] = acc[o].x;
+        d1[o] = acc[o].y;
+      }
+    }
+  } else {
   for (int cb = warp; cb < C * NB2; cb += kNW) {
     const int j = lane;
     const int ib = cb % NB2;
@@ -222,6 +273,7 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
     T* dst = res + (c * OY + j) * OP + ib * kRB;
 #pragma unroll
     for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
+  }
   }
   return res;
 }

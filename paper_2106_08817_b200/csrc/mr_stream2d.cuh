@@ -31,7 +31,7 @@ struct StreamCfg {
   static constexpr int PXZ = round_up(RX + A - 1, A);      // z box width
   static constexpr int PP = (RX % 2) ? RX : RX + 1;        // product pitch (odd)
   static constexpr int RING = G + 2 * R;  // filtered rows kept
-  static constexpr int RP = OX + 1;       // ring pitch (odd)
+  static constexpr int RP = OX + 2;       // ring pitch (even: 8-byte column pairs)
   // smem layout (elements after the 128-B head)
   static constexpr int o_ist = 0;
   static constexpr int n_ist = round_up((G + 2) * PXI + A, 32);
@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kThreads)
   using C = StreamCfg<T, R>;
   constexpr int OX = C::OX, G = C::G, RX = C::RX, PXI = C::PXI, PXZ = C::PXZ, PP = C::PP,
                 RING = C::RING, RP = C::RP;
+  static_assert(sizeof(T) == 4 && OX == 64 && G == 32, "fp32 FFMA2 layout");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   T* base = reinterpret_cast<T*>(smem_raw + C::head);
@@ -148,28 +149,35 @@ __global__ void __launch_bounds__(kThreads)
             }
           __syncthreads();
         }
-        // ---- horizontal FIR of the new rows -> ring (lanes <-> rows) ----
+        // ---- horizontal FIR of the new rows -> ring: rows (r, r+16) per thread (FFMA2) ----
         constexpr int NB = OX / kRB;
-        for (int cb = warp; cb < 2 * NB; cb += kNW) {
-          const int r = lane;
+        for (int cb = warp; cb < NB; cb += kNW) {  // (c, column-block pair)
+          const int r = lane & 15;
+          const int ib = 2 * (cb % (NB / 2)) + (lane >> 4);
+          const int c = cb / (NB / 2);
           if (r >= cin) continue;
-          const int ib = cb % NB, c = cb / NB;
-          const T* src = P + c * G * PP + r * PP + ib * kRB;
-          T acc[kRB];
+          const T* s0 = P + c * G * PP + r * PP + ib * kRB;
+          const T* s1 = s0 + 16 * PP;
+          float2 acc[kRB];
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+          for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
           for (int t = 0; t < kRB + 2 * R; ++t) {
-            const T x = src[t];
+            const float2 x = make_float2(s0[t], s1[t]);
 #pragma unroll
             for (int o = 0; o < kRB; ++o) {
               const int tap = t - o;
-              if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+              if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
             }
           }
-          T* dst = ring + c * RING * RP + (u0 + r - ring_lo) * RP + ib * kRB;
+          T* d0 = ring + c * RING * RP + (u0 + r - ring_lo) * RP + ib * kRB;
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
+          for (int o = 0; o < kRB; ++o) d0[o] = acc[o].x;
+          if (r + 16 < cin) {
+            T* d1 = d0 + 16 * RP;
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) d1[o] = acc[o].y;
+          }
         }
         __syncthreads();
         if (u0 == 0) {  // rows above the image replicate row 0 (only in the first block)
@@ -202,35 +210,39 @@ __global__ void __launch_bounds__(kThreads)
       next_u = u0 + cnt;
     }
 
-    // ---- vertical FIR over the ring for output rows [y0, y0+G) (lanes <-> columns) ----
+    // ---- vertical FIR over the ring for output rows [y0, y0+G): lanes <-> column pairs ----
     constexpr int NBV = G / kRB;
     for (int cb = warp; cb < 2 * NBV; cb += kNW) {
       const int jb = cb % NBV, c = cb / NBV;
-      for (int i = lane; i < OX; i += 32) {
-        const T* src = ring + c * RING * RP + (y0 + jb * kRB - R - ring_lo) * RP + i;
-        T acc[kRB];
+      const int i = 2 * lane;  // OX == 64: one column pair per lane
+      const float2* src = reinterpret_cast<const float2*>(
+          ring + c * RING * RP + (y0 + jb * kRB - R - ring_lo) * RP + i);
+      float2 acc[kRB];
 #pragma unroll
-        for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < kRB + 2 * R; ++t) {
-          const T x = src[t * RP];
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const float2 x = src[t * (RP / 2)];
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) {
-            const int tap = t - o;
-            if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
-          }
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
         }
-        const int gx = x0 + i;
-        if (gx < W) {
-          T* vo = (c == 0 ? v0 : v1) + gx;
+      }
+      const int gx = x0 + i;
+      T* vo = (c == 0 ? v0 : v1) + gx;
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) {
-            const int gy = y0 + jb * kRB + o;
-            if (gy < H) {
-              const T val = -acc[o];
-              vo[(long long)gy * W] = val;
-              flags |= guard_bits(val, MR_GUARD_VELOCITY_NONFINITE);
-            }
+      for (int o = 0; o < kRB; ++o) {
+        const int gy = y0 + jb * kRB + o;
+        if (gy < H) {
+          const T a0 = -acc[o].x, a1 = -acc[o].y;
+          if (gx < W) {
+            vo[(long long)gy * W] = a0;
+            flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
+          }
+          if (gx + 1 < W) {
+            vo[(long long)gy * W + 1] = a1;
+            flags |= guard_bits(a1, MR_GUARD_VELOCITY_NONFINITE);
           }
         }
       }
