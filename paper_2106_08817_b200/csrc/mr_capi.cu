@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "mr_launch.cuh"
+#include "mr_tma.h"
+#include "mr_transport2d.cuh"
 
 namespace mr {
 
@@ -148,6 +150,20 @@ static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, co
   StepArgs<T> a{I,     z,       v,      In,        zn,          phi_in,
                 phi_out, (T)dt, (T)(dt * mu), mu != 0.0, guard_in, guard_out,
                 guard_stride, g};
+  {  // TMA-staged tile variant when the layout is TMA-describable
+    using C = TrCfg<T>;
+    StepMaps m;
+    if (make_map3<T>(&m.I, I, g.W, g.H, g.B, C::GX, C::GY) &&
+        make_map3<T>(&m.z, z, g.W, g.H, g.B, C::GX, C::GY) &&
+        make_map3<T>(&m.v, v, g.W, g.H, 2LL * g.B, C::VX, C::VY)) {
+      static const cudaError_t attr = cudaFuncSetAttribute(
+          k_sl_step2d_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
+      if (attr != cudaSuccess) return cuda_status(attr);
+      dim3 grid((g.W + C::TX - 1) / C::TX, (g.H + C::TY - 1) / C::TY, g.B);
+      k_sl_step2d_tma<T><<<grid, kThreads, C::bytes, s>>>(a, m);
+      return cuda_status(cudaGetLastError());
+    }
+  }
   dim3 grid((g.W + 31) / 32, (g.H + kStepRows - 1) / kStepRows, g.B);
   k_sl_step2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
