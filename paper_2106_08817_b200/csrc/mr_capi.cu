@@ -174,6 +174,23 @@ static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I,
                                const T* v, const T* ibar, const T* zbar, T* ib, T* zb, T* vbar,
                                cudaStream_t s, double reg_lam = 0.0) {
   AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, (T)reg_lam, g};
+  {  // TMA-staged tile variant when the layout is TMA-describable
+    using C = TrCfg<T>;
+    AdjMaps m;
+    if (make_map3<T>(&m.I, I, g.W, g.H, g.B, C::GX, C::GY) &&
+        make_map3<T>(&m.z, z, g.W, g.H, g.B, C::GX, C::GY) &&
+        make_map3<T>(&m.v, v, g.W, g.H, 2LL * g.B, C::VX, C::VY) &&
+        make_map3<T>(&m.ibar, ibar, g.W, g.H, g.B, C::VX, C::VY) &&
+        make_map3<T>(&m.zbar, zbar, g.W, g.H, g.B, C::VX, C::VY)) {
+      constexpr size_t bytes = AdjCfg<T>::bytes;
+      static const cudaError_t attr = cudaFuncSetAttribute(
+          k_sl_adjoint2d_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (attr != cudaSuccess) return cuda_status(attr);
+      dim3 grid((g.W + C::TX - 1) / C::TX, (g.H + C::TY - 1) / C::TY, g.B);
+      k_sl_adjoint2d_tma<T><<<grid, kThreads, bytes, s>>>(a, m);
+      return cuda_status(cudaGetLastError());
+    }
+  }
   dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjRows - 1) / kAdjRows, g.B);
   k_sl_adjoint2d<T><<<grid, kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());

@@ -124,3 +124,194 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 }  // namespace mr
+
+namespace mr {
+
+// ---------------------------------------------------------------------------------
+// TMA-staged adjoint of one SL step (objective.py:118-147), K3.  Window of I, z
+// (HB halo, for the gathers) and of v, ibar, zbar (1-px halo: divergence, and the
+// divergence-adjoint seed s on the tile's ring) staged by TMA; phase 1 computes s
+// for owners and ring and issues the warp-merged scatters; phase 2 recomputes the
+// (smem-cheap) plans and writes vbar with D^T s from shared memory.
+// ---------------------------------------------------------------------------------
+struct AdjMaps {
+  CUtensorMap I, z, v, ibar, zbar;
+};
+
+template <typename T>
+struct AdjCfg {
+  using C = TrCfg<T>;
+  static constexpr int nG = C::nG, nV = C::nV;
+  static constexpr int nS = round_up((C::TY + 2) * (C::TX + 2), 32);
+  static constexpr size_t bytes = C::head + sizeof(T) * (size_t)(2 * nG + 4 * nV + nS);
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    k_sl_adjoint2d_tma(AdjArgs<T> a, const __grid_constant__ AdjMaps maps) {
+  using C = TrCfg<T>;
+  using AC = AdjCfg<T>;
+  constexpr int TX = C::TX, TY = C::TY, HB = C::HB, GX = C::GX, VX = C::VX, SX = TX + 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  T* sI0 = reinterpret_cast<T*>(smem_raw + C::head);
+  T* sz0 = sI0 + C::nG;
+  T* sv00 = sz0 + C::nG;
+  T* sv10 = sv00 + C::nV;
+  T* sib0 = sv10 + C::nV;
+  T* szb0 = sib0 + C::nV;
+  T* s_div = szb0 + C::nV;  // [(TY+2)][(TX+2)], s = -dt * zbar * B(z)
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int gx0 = x0 - HB, gy0 = y0 - HB;
+  const int offG = align_shift(gx0, C::A), offV = align_shift(x0 - 1, C::A);
+  const T* sI = sI0 + offG;
+  const T* sz = sz0 + offG;
+  const T* sv0 = sv00 + offV;   // (r, c) <-> image (y0-1+r, x0-1+c)
+  const T* sv1 = sv10 + offV;
+  const T* sib = sib0 + offV;
+  const T* szb = szb0 + offV;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(bar, (unsigned)(sizeof(T) * (2 * GX * C::GY + 4 * VX * C::VY)));
+    tma_load_3d(sI0, &maps.I, gx0 - offG, gy0, b, bar);
+    tma_load_3d(sz0, &maps.z, gx0 - offG, gy0, b, bar);
+    tma_load_3d(sv00, &maps.v, x0 - 1 - offV, y0 - 1, 2 * b, bar);
+    tma_load_3d(sv10, &maps.v, x0 - 1 - offV, y0 - 1, 2 * b + 1, bar);
+    tma_load_3d(sib0, &maps.ibar, x0 - 1 - offV, y0 - 1, b, bar);
+    tma_load_3d(szb0, &maps.zbar, x0 - 1 - offV, y0 - 1, b, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+
+  const T* __restrict__ I = a.I + b * N;
+  const T* __restrict__ z = a.z + b * N;
+  const T dt = a.dt;
+
+  // corners of I or z at the foot of window pixel (r, c) (v-window coordinates)
+  auto corners = [&](const T* sf, const T* __restrict__ gf, const AxisPlan<T>& py,
+                     const AxisPlan<T>& px, T& ca, T& cb, T& cc, T& cd) {
+    const int ry = py.i0 - gy0, rx = px.i0 - gx0;
+    if (ry >= 0 && ry + 1 < C::GY && rx >= 0 && rx + 1 < TX + 2 * HB) {
+      const int e = ry * GX + rx;
+      ca = sf[e]; cb = sf[e + GX]; cc = sf[e + 1]; cd = sf[e + GX + 1];
+    } else {
+      const long long c00 = (long long)py.i0 * W + px.i0;
+      ca = gf[c00]; cb = gf[c00 + W]; cc = gf[c00 + 1]; cd = gf[c00 + W + 1];
+    }
+  };
+
+  // ---- s on the ring (1-px halo) ----
+  constexpr int NRING = 2 * (TX + 2) + 2 * TY;
+  for (int h = threadIdx.x; h < NRING; h += kThreads) {
+    int j, i;
+    if (h < TX + 2) { j = 0; i = h; }
+    else if (h < 2 * (TX + 2)) { j = TY + 1; i = h - (TX + 2); }
+    else { const int kk = h - 2 * (TX + 2); j = 1 + (kk >> 1); i = (kk & 1) ? TX + 1 : 0; }
+    const int gy = y0 - 1 + j, gx = x0 - 1 + i;
+    T sv = T(0);
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+      const int vi = j * VX + i;
+      const AxisPlan<T> hy = plan_axis<T>(gy, sv0[vi], dt, H);
+      const AxisPlan<T> hx = plan_axis<T>(gx, sv1[vi], dt, W);
+      T za, zb2, zc, zd;
+      corners(sz, z, hy, hx, za, zb2, zc, zd);
+      sv = -dt * (szb[vi] * bilerp(za, zb2, zc, zd, hy.f, hx.f));
+    }
+    s_div[j * SX + i] = sv;
+  }
+
+  // ---- phase 1: owners' s and the scatters (warp-merged, lanes = consecutive x) ----
+  T* __restrict__ ibo = a.ib + b * N;
+  T* __restrict__ zbo = a.zb + b * N;
+  constexpr int CPR = TX / 32;
+#pragma unroll 1
+  for (int k = 0; k < C::PIX; ++k) {
+    const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
+    const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
+    const int x = x0 + tx, y = y0 + ty;
+    const bool own = x < W && y < H;
+    const int vi = (ty + 1) * VX + tx + 1;
+    const T vy = sv0[vi], vx = sv1[vi];
+    const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
+    const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
+    T za = T(0), zb2 = T(0), zc = T(0), zd = T(0);
+    if (own) corners(sz, z, py, px, za, zb2, zc, zd);
+    const T ib_ = sib[vi], zb_ = szb[vi];
+    T scale = T(1);
+    if (own) {
+      const T up = (y > 0) ? sv0[vi - VX] : vy;
+      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+      const T lf = (x > 0) ? sv1[vi - 1] : vx;
+      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+      scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
+    }
+    s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * bilerp(za, zb2, zc, zd, py.f, px.f)) : T(0);
+    const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
+    const T wz = zb_ * scale;
+    const long long c00 = (long long)py.i0 * W + px.i0;
+    scatter4_merged(ibo, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
+                    fy * fx * ib_);
+    scatter4_merged(zbo, c00, own, (long long)W, wy * wx * wz, fy * wx * wz, wy * fx * wz,
+                    fy * fx * wz);
+    if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
+  }
+  __syncthreads();
+
+  // ---- phase 2: vbar (objective.py:131-132, 143-147) ----
+#pragma unroll 1
+  for (int k = 0; k < C::PIX; ++k) {
+    const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
+    const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) continue;
+    const int vi = (ty + 1) * VX + tx + 1;
+    const T vy = sv0[vi], vx = sv1[vi];
+    const AxisPlan<T> py = plan_axis<T>(y, vy, dt, H);
+    const AxisPlan<T> px = plan_axis<T>(x, vx, dt, W);
+    T ia, ib2, ic, id, za, zb2, zc, zd;
+    corners(sI, I, py, px, ia, ib2, ic, id);
+    corners(sz, z, py, px, za, zb2, zc, zd);
+    const T ib_ = sib[vi], zb_ = szb[vi];
+    const T up = (y > 0) ? sv0[vi - VX] : vy;
+    const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+    const T lf = (x > 0) ? sv1[vi - 1] : vx;
+    const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+    const T wz = zb_ * (T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W)));
+    const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
+    const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
+    const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
+    T vb0 = -dt * ddy * ib_;
+    T vb1 = -dt * ddx * ib_;
+    const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
+    const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
+    vb0 += -dt * dzy * wz;
+    vb1 += -dt * dzx * wz;
+    const int j = ty + 1, i = tx + 1;
+    const T sm_ = s_div[(j - 1) * SX + i], sp_ = s_div[(j + 1) * SX + i];
+    const T s_first_y = (y <= 1) ? s_div[(j - y) * SX + i] : T(0);
+    const T s_last_y = (y >= H - 2) ? s_div[(j + (H - 1 - y)) * SX + i] : T(0);
+    vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+    const T sl_ = s_div[j * SX + i - 1], sr_ = s_div[j * SX + i + 1];
+    const T s_first_x = (x <= 1) ? s_div[j * SX + i - x] : T(0);
+    const T s_last_x = (x >= W - 2) ? s_div[j * SX + i + (W - 1 - x)] : T(0);
+    vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    const long long q = (long long)y * W + x;
+    if (a.reg_lam != T(0)) {  // k = 0: fold -lam*m0
+      const int ce = (ty + HB) * GX + tx + HB;
+      const T c = sI[ce];
+      const T g0 = grad1(sI[ce - GX], c, sI[ce + GX], y, H);
+      const T g1 = grad1(sI[ce - 1], c, sI[ce + 1], x, W);
+      const T zz = sz[ce];
+      vb0 = vb0 - a.reg_lam * (zz * g0);
+      vb1 = vb1 - a.reg_lam * (zz * g1);
+    }
+    a.vbar[b * 2 * N + q] = vb0;
+    a.vbar[b * 2 * N + N + q] = vb1;
+  }
+}
+
+}  // namespace mr
