@@ -69,7 +69,7 @@ def shard(n: int, rank: int, world: int) -> list:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled (every 100 ms) during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -78,31 +78,32 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                return
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land inside the region
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self._p is None:
+            return
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
 
     def summary(self):
         if not self.rows:
@@ -242,7 +243,8 @@ def run_ours(args):
             "alg_bytes_per_voxel": ab[dom] if dom in ab else sum(ab.values()) * T,
             "avg_launch_ms": kt[dom],
             "share_of_step": share[dom],
-            "traffic": None,
+            "traffic": kernel_traffic(dom),
+            "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/r01_traffic.json)",
         },
         "step_roofline": {
             "alg_bytes_per_voxel_step": sum(ab.values()),
@@ -265,6 +267,24 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+NCU_NAMES = {"velocity": "k_velocity2d_stream", "velocity_adjoint": "k_velocity_adj2d<",
+             "sl_adjoint": "k_sl_adjoint2d_tma", "sl_step": "k_sl_step2d_tma"}
+
+
+def kernel_traffic(kernel: str):
+    """DRAM bytes per launch of a bench kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+            tr = json.load(f)
+    except Exception:
+        return None
+    key = NCU_NAMES.get(kernel)
+    for name, d in tr.items():
+        if key and key in name:
+            return d["dram_bytes"]
+    return None
 
 
 def kernel_times(bg, w, stream, reps: int = 1) -> dict:
