@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     return p.parse_args()
 
 
@@ -157,8 +158,13 @@ def run_ours(args):
             torch.as_tensor(c.z0, dtype=dtype))
     stream = torch.cuda.current_stream()
 
+    # the whole grad (2T+1 forward + 2T+2 adjoint launches) replays as one CUDA graph
+    step = bg.run
+    if not args.no_graph:
+        bg.capture_graph()
+        step = bg.replay
     for _ in range(args.warmup):
-        bg.run()
+        step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -167,7 +173,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            bg.run()
+            step()
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -225,6 +231,7 @@ def run_ours(args):
             "workload": f"{c.name}: {B_global} pairs x {'x'.join(map(str, c.shape))}, T={T}, "
                         f"sigma={c.sigma}, r={c.radius}, mu={c.mu}, grad() = shoot + adjoint",
             "momentum_scale": c.manifest.get("momentum_scale"),
+            "cuda_graph": not args.no_graph,
             "global_batch": B_global,
             "shape": list(c.shape),
             "n_steps": T,

@@ -20,6 +20,8 @@ int velocity_stream_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStrea
   } else {
   using C = StreamCfg<T, R>;
   if (C::bytes > 227 * 1024) return 1;
+  // one CTA per strip walks all rows: only worth it with >= 2 strips per SM
+  if ((long long)((g.W + C::OX - 1) / C::OX) * g.B < 2LL * 148) return 1;
   CUtensorMap mI, mZ;
   if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, C::PXI, C::G + 2) ||
       !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, C::PXZ, C::G))

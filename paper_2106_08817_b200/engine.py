@@ -279,6 +279,25 @@ class BatchGrad:
                       self.bufs, stream)
         return self.bufs
 
+    def capture_graph(self):
+        """Capture one run() (all forward and adjoint launches) in a CUDA graph.
+
+        Buffers and tensor maps are fixed at capture time, so replays read the
+        current contents of traj.I[0], traj.z[0] and target.  Warm up first so
+        the one-time kernel attribute setup happens outside the capture.
+        """
+        self.run()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.run()
+        torch.cuda.synchronize()
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+        return self.bufs
+
     def launches_per_run(self) -> int:
         """Kernels of ours per run() (memsets excluded)."""
         T = self.n_steps
