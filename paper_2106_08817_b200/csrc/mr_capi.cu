@@ -109,6 +109,10 @@ static long long scalars(const mr_grid& g) {
   return (long long)g.batch * g.n[0] * g.n[1] * (g.ndim == 3 ? g.n[2] : 1);
 }
 
+static dim3 grid3d(const Grid3& g) {
+  return dim3((unsigned)((g.W + 31) / 32), (unsigned)((g.H + 7) / 8), (unsigned)(g.B * g.D));
+}
+
 static unsigned flat_blocks(long long n) {
   long long b = (n + kThreads - 1) / kThreads;
   return (unsigned)(b < 148LL * 16 ? b : 148LL * 16);
@@ -121,7 +125,7 @@ static unsigned flat_blocks(long long n) {
 template <typename T>
 static int velocity3d(const Grid3& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
                       T* tmp, int32_t* guard, int guard_stride, cudaStream_t s) {
-  k_product3d<T><<<flat_blocks((long long)g.B * g.N), kThreads, 0, s>>>(I, z, v, g);
+  k_product3d<T><<<grid3d(g), kThreads, 0, s>>>(I, z, v, g);
   int rc = cuda_status(cudaGetLastError());
   if (rc) return rc;
   Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};  // every (pair, component, slice) as a 2D image
@@ -137,7 +141,7 @@ static int sl_step3d(const Grid3& g, double dt, double mu, const T* I, const T* 
                      int guard_stride = 1) {
   Step3Args<T> a{I,       z,      v,        In,          zn,      phi_in,    phi_out,
                  (T)dt,   (T)(dt * mu), mu != 0.0, guard_in, guard_out, guard_stride, g};
-  k_sl_step3d<T><<<flat_blocks((long long)g.B * g.N), kThreads, 0, s>>>(a);
+  k_sl_step3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
   return cuda_status(cudaGetLastError());
 }
 
@@ -324,7 +328,6 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
   int rc = cost_terms3d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
   if (rc) return check_rc(rc, "cost_terms3d");
   if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
-  const unsigned nb = flat_blocks(S1);
   for (int step = T_ - 1; step >= 0; --step) {
     if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
     Adj3Args<T> a{};
@@ -343,8 +346,8 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
     a.has_mu = mu != 0.0;
     a.reg_lam = (T)(step == 0 ? lam : 0.0);
     a.g = g;
-    k_divseed3d<T><<<nb, kThreads, 0, s>>>(a);
-    k_sl_adjoint3d<T><<<nb, kThreads, 0, s>>>(a);
+    k_divseed3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
+    k_sl_adjoint3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
     if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "sl_adjoint3d");
     // ktv = K^T vbar: axis 0 first, then axes 1, 2 per slice (kernel.py:76-79 order)
     rc = launch_fir_axis0<T>(k.radius, tp, vbar, tmp, g.B * 3, g.D, g.HW, true, 0, nullptr, 1, s);
@@ -364,9 +367,9 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
       e.v0 = v;
       e.zout = zbar0;
       e.flags = flags;
-      k_veladj_epi3d<T, true><<<nb, kThreads, 0, s>>>(e);
+      k_veladj_epi3d<T, true><<<grid3d(g), kThreads, 0, s>>>(e);
     } else {
-      k_veladj_epi3d<T, false><<<nb, kThreads, 0, s>>>(e);
+      k_veladj_epi3d<T, false><<<grid3d(g), kThreads, 0, s>>>(e);
     }
     if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "veladj_epi3d");
     T* t = cur;

@@ -24,6 +24,25 @@ struct Grid3 {
   long long HW;  // H*W
 };
 
+// Elementwise 3D kernels run on a 3D grid: blockIdx.x -> 32 columns, blockIdx.y ->
+// 8 rows, blockIdx.z -> (pair, slice); threadIdx.x = 32 x 8.  No index divisions.
+struct Vox {
+  int b, d, y, x;
+  int q;        // in-pair linear index (N < 2^31)
+  bool ok;
+};
+
+__device__ __forceinline__ Vox vox3(const Grid3& g) {
+  Vox v;
+  v.x = blockIdx.x * 32 + (threadIdx.x & 31);
+  v.y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  v.b = blockIdx.z / g.D;
+  v.d = blockIdx.z - v.b * g.D;
+  v.ok = v.x < g.W && v.y < g.H;
+  v.q = (v.d * g.H + (v.ok ? v.y : 0)) * g.W + (v.ok ? v.x : 0);
+  return v;
+}
+
 __device__ __forceinline__ void coords3(long long q, const Grid3& g, int& d, int& y, int& x) {
   d = (int)(q / g.HW);
   long long r = q - (long long)d * g.HW;
@@ -36,7 +55,7 @@ template <typename T>
 __device__ __forceinline__ void grad3(const T* __restrict__ f, long long q, int d, int y, int x,
                                       const Grid3& g, T& g0, T& g1, T& g2) {
   const T c = f[q];
-  const long long HW = g.HW;
+  const int HW = (int)g.HW;
   g0 = grad1(d > 0 ? f[q - HW] : c, c, d < g.D - 1 ? f[q + HW] : c, d, g.D);
   g1 = grad1(y > 0 ? f[q - g.W] : c, c, y < g.H - 1 ? f[q + g.W] : c, y, g.H);
   g2 = grad1(x > 0 ? f[q - 1] : c, c, x < g.W - 1 ? f[q + 1] : c, x, g.W);
@@ -49,20 +68,16 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) k_product3d(const T* __restrict__ I,
                                                          const T* __restrict__ z, T* out,
                                                          Grid3 g) {
-  const long long total = (long long)g.B * g.N;
-  for (long long p = blockIdx.x * (long long)kThreads + threadIdx.x; p < total;
-       p += (long long)gridDim.x * kThreads) {
-    const long long b = p / g.N, q = p - b * g.N;
-    int d, y, x;
-    coords3(q, g, d, y, x);
-    T g0, g1, g2;
-    grad3(I + b * g.N, q, d, y, x, g, g0, g1, g2);
-    const T zz = z[p];
-    T* o = out + b * 3 * g.N + q;
-    o[0] = zz * g0;
-    o[g.N] = zz * g1;
-    o[2 * g.N] = zz * g2;
-  }
+  const Vox v = vox3(g);
+  if (!v.ok) return;
+  const long long base = (long long)v.b * g.N;
+  T g0, g1, g2;
+  grad3(I + base, v.q, v.d, v.y, v.x, g, g0, g1, g2);
+  const T zz = z[base + v.q];
+  T* o = out + (long long)v.b * 3 * g.N + v.q;
+  o[0] = zz * g0;
+  o[g.N] = zz * g1;
+  o[2 * g.N] = zz * g2;
 }
 
 // ------------------------------------------------------------------------------
@@ -268,47 +283,46 @@ struct Step3Args {
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_step3d(Step3Args<T> a) {
   const Grid3 g = a.g;
-  const long long total = (long long)g.B * g.N;
-  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
-       pp += (long long)gridDim.x * kThreads) {
-    const long long b = pp / g.N, q = pp - b * g.N;
-    int d, y, x;
-    coords3(q, g, d, y, x);
-    const T* __restrict__ I = a.I + b * g.N;
-    const T* __restrict__ z = a.z + b * g.N;
-    const T* __restrict__ v0 = a.v + b * 3 * g.N;
-    const T* __restrict__ v1 = v0 + g.N;
-    const T* __restrict__ v2 = v1 + g.N;
-    const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
-    const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
-    if (a.guard_in) {
-      const unsigned fin = guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE) |
-                           guard_bits(z[q], MR_GUARD_MOMENTUM_NONFINITE);
-      if (fin) atomicOr(reinterpret_cast<int*>(a.guard_in + b * a.guard_stride), (int)fin);
-    }
-    T cv[8];
-    corners8(I, p, g, cv);
-    T bi = trilerp(cv, p);
-    if (a.has_mu) bi = bi + a.dtmu * z[q];
-    corners8(z, p, g, cv);
-    const T bz = trilerp(cv, p);
-    const T div = grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
-                  grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
-                  grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
-    const T zn = bz * (T(1) - a.dt * div);
-    a.In[pp] = bi;
-    a.zn[pp] = zn;
-    if (a.guard_out) {
-      const unsigned fo = guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) |
-                          guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
-      if (fo) atomicOr(reinterpret_cast<int*>(a.guard_out + b * a.guard_stride), (int)fo);
-    }
-    if (a.phi_in) {
+  const Vox vx_ = vox3(g);
+  if (!vx_.ok) return;
+  const int d = vx_.d, y = vx_.y, x = vx_.x, q = vx_.q;
+  const long long b = vx_.b;
+  const T* __restrict__ I = a.I + b * g.N;
+  const T* __restrict__ z = a.z + b * g.N;
+  const T* __restrict__ v0 = a.v + b * 3 * g.N;
+  const T* __restrict__ v1 = v0 + g.N;
+  const T* __restrict__ v2 = v1 + g.N;
+  const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
+  const T up = d > 0 ? v0[q - g.HW] : a0, dn = d < g.D - 1 ? v0[q + g.HW] : a0;
+  const T nn = y > 0 ? v1[q - g.W] : a1, ss = y < g.H - 1 ? v1[q + g.W] : a1;
+  const T lf = x > 0 ? v2[q - 1] : a2, rt = x < g.W - 1 ? v2[q + 1] : a2;
+  const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
+  T ci[8], cz[8];
+  corners8(I, p, g, ci);
+  corners8(z, p, g, cz);
+  const T zq = (a.has_mu || a.guard_in) ? z[q] : T(0);
+  if (a.guard_in) {
+    const unsigned fin = guard_bits(I[q], MR_GUARD_IMAGE_NONFINITE) |
+                         guard_bits(zq, MR_GUARD_MOMENTUM_NONFINITE);
+    if (fin) atomicOr(reinterpret_cast<int*>(a.guard_in + b * a.guard_stride), (int)fin);
+  }
+  T bi = trilerp(ci, p);
+  if (a.has_mu) bi = bi + a.dtmu * zq;
+  const T bz = trilerp(cz, p);
+  const T div = grad1(up, a0, dn, d, g.D) + grad1(nn, a1, ss, y, g.H) + grad1(lf, a2, rt, x, g.W);
+  const T zn = bz * (T(1) - a.dt * div);
+  a.In[b * g.N + q] = bi;
+  a.zn[b * g.N + q] = zn;
+  if (a.guard_out) {
+    const unsigned fo = guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) |
+                        guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+    if (fo) atomicOr(reinterpret_cast<int*>(a.guard_out + b * a.guard_stride), (int)fo);
+  }
+  if (a.phi_in) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        corners8(a.phi_in + (b * 3 + c) * g.N, p, g, cv);
-        a.phi_out[(b * 3 + c) * g.N + q] = trilerp(cv, p);
-      }
+    for (int c = 0; c < 3; ++c) {
+      corners8(a.phi_in + (b * 3 + c) * g.N, p, g, ci);
+      a.phi_out[(b * 3 + c) * g.N + q] = trilerp(ci, p);
     }
   }
 }
@@ -353,91 +367,112 @@ struct Adj3Args {
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_divseed3d(Adj3Args<T> a) {
   const Grid3 g = a.g;
-  const long long total = (long long)g.B * g.N;
-  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
-       pp += (long long)gridDim.x * kThreads) {
-    const long long b = pp / g.N, q = pp - b * g.N;
-    int d, y, x;
-    coords3(q, g, d, y, x);
-    const T* __restrict__ v0 = a.v + b * 3 * g.N;
-    const Plan3<T> p = plan3<T>(d, y, x, v0[q], v0[g.N + q], v0[2 * g.N + q], a.dt, g);
-    T cv[8];
-    corners8(a.z + b * g.N, p, g, cv);
-    a.s_out[pp] = -a.dt * (a.zbar[pp] * trilerp(cv, p));
+  const Vox v = vox3(g);
+  if (!v.ok) return;
+  const long long b = v.b;
+  const T* __restrict__ v0 = a.v + b * 3 * g.N;
+  const Plan3<T> p = plan3<T>(v.d, v.y, v.x, v0[v.q], v0[g.N + v.q], v0[2 * g.N + v.q], a.dt, g);
+  T cv[8];
+  corners8(a.z + b * g.N, p, g, cv);
+  a.s_out[b * g.N + v.q] = -a.dt * (a.zbar[b * g.N + v.q] * trilerp(cv, p));
+}
+
+// Scatter of the 8 trilinear-transpose contributions with warp-level merging of
+// x-adjacent cells (lanes are consecutive x): where lane l-1's +x cells are
+// lane l's cells, lane l adds them and lane l-1 skips its own (4 of 8 REDs).
+template <typename T>
+__device__ __forceinline__ void scatter8_merged(T* __restrict__ out, int base, bool valid,
+                                                const Grid3& g, const T w[8]) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? base : -4;
+  const int prev_key = __shfl_up_sync(full, key, 1);
+  const int next_key = __shfl_down_sync(full, key, 1);
+  const bool merge_left = lane > 0 && prev_key >= 0 && prev_key + 1 == key;
+  const bool merged_by_next = lane < 31 && next_key >= 0 && key + 1 == next_key;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // corners c (x bit 0) pair with c | 4 (x bit 1)
+    const int off = ((c & 1) ? (int)g.HW : 0) + ((c & 2) ? g.W : 0);
+    const T pr = __shfl_up_sync(full, w[c | 4], 1);
+    if (valid) {
+      atomicAdd(out + base + off, merge_left ? w[c] + pr : w[c]);
+      if (!merged_by_next) atomicAdd(out + base + off + 1, w[c | 4]);
+    }
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   const Grid3 g = a.g;
-  const long long total = (long long)g.B * g.N;
-  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
-       pp += (long long)gridDim.x * kThreads) {
-    const long long b = pp / g.N, q = pp - b * g.N;
-    int d, y, x;
-    coords3(q, g, d, y, x);
-    const T* __restrict__ I = a.I + b * g.N;
-    const T* __restrict__ z = a.z + b * g.N;
-    const T* __restrict__ v0 = a.v + b * 3 * g.N;
-    const T* __restrict__ v1 = v0 + g.N;
-    const T* __restrict__ v2 = v1 + g.N;
-    const T* __restrict__ s = a.s + b * g.N;
-    const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
-    const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
-    const T ib_ = a.ibar[pp], zb_ = a.zbar[pp];
-    T* __restrict__ ibo = a.ib + b * g.N;
-    T* __restrict__ zbo = a.zb + b * g.N;
-    T w8[8];
+  const Vox vx_ = vox3(g);
+  const bool own = vx_.ok;
+  const int d = vx_.d, y = own ? vx_.y : 0, x = own ? vx_.x : 0, q = vx_.q;
+  const long long b = vx_.b;
+  const T* __restrict__ I = a.I + b * g.N;
+  const T* __restrict__ z = a.z + b * g.N;
+  const T* __restrict__ v0 = a.v + b * 3 * g.N;
+  const T* __restrict__ v1 = v0 + g.N;
+  const T* __restrict__ v2 = v1 + g.N;
+  const T* __restrict__ s = a.s + b * g.N;
+  const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
+  const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
+  const int base = (int)p.base;
+  const T ib_ = a.ibar[b * g.N + q], zb_ = a.zbar[b * g.N + q];
+  T w8[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) w8[c] = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
+  for (int c = 0; c < 8; ++c) w8[c] = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
+  const T div =
+      grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
+      grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
+      grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
+  const T wz = zb_ * (T(1) - a.dt * div);
+  T* __restrict__ ibo = a.ib + b * g.N;
+  T* __restrict__ zbo = a.zb + b * g.N;
+  T cw[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) atomicAdd(ibo + p.base + corner_off<T>(c, g), w8[c] * ib_);
-    T cv[8], dI[3], dz[3];
-    corners8(I, p, g, cv);
-    coord_grad3(cv, p, dI);
-    T vb[3];
+  for (int c = 0; c < 8; ++c) cw[c] = w8[c] * ib_;
+  scatter8_merged(ibo, base, own, g, cw);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
-    const T div =
-        grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
-        grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
-        grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
-    const T wz = zb_ * (T(1) - a.dt * div);
-    if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
+  for (int c = 0; c < 8; ++c) cw[c] = w8[c] * wz;
+  scatter8_merged(zbo, base, own, g, cw);
+  if (!own) return;
+  if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
+  T cv[8], dI[3], dz[3];
+  corners8(I, p, g, cv);
+  coord_grad3(cv, p, dI);
+  corners8(z, p, g, cv);
+  coord_grad3(cv, p, dz);
+  T vb[3];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) atomicAdd(zbo + p.base + corner_off<T>(c, g), w8[c] * wz);
-    corners8(z, p, g, cv);
-    coord_grad3(cv, p, dz);
+  for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
-    // vbar_c += D_c^T s (gather form along each axis)
-    {
-      const long long st[3] = {g.HW, (long long)g.W, 1};
-      const int pos[3] = {d, y, x};
-      const int n[3] = {g.D, g.H, g.W};
+  for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
+  {  // vbar_c += D_c^T s (gather form along each axis)
+    const int st[3] = {(int)g.HW, g.W, 1};
+    const int pos[3] = {d, y, x};
+    const int n[3] = {g.D, g.H, g.W};
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int j = pos[c];
-        const T sm = j > 0 ? s[q - st[c]] : T(0);
-        const T sp = j < n[c] - 1 ? s[q + st[c]] : T(0);
-        const T sf = j == 0 ? s[q] : (j == 1 ? sm : T(0));
-        const T sl = j == n[c] - 1 ? s[q] : (j == n[c] - 2 ? sp : T(0));
-        vb[c] += diff_adj1(sm, sp, sf, sl, j, n[c]);
-      }
+    for (int c = 0; c < 3; ++c) {
+      const int j = pos[c];
+      const T sm = j > 0 ? s[q - st[c]] : T(0);
+      const T sp = j < n[c] - 1 ? s[q + st[c]] : T(0);
+      const T sf = j == 0 ? s[q] : (j == 1 ? sm : T(0));
+      const T sl = j == n[c] - 1 ? s[q] : (j == n[c] - 2 ? sp : T(0));
+      vb[c] += diff_adj1(sm, sp, sf, sl, j, n[c]);
     }
-    if (a.reg_lam != T(0)) {
-      T g0, g1, g2;
-      grad3(I, q, d, y, x, g, g0, g1, g2);
-      const T zz = z[q];
-      vb[0] = vb[0] - a.reg_lam * (zz * g0);
-      vb[1] = vb[1] - a.reg_lam * (zz * g1);
-      vb[2] = vb[2] - a.reg_lam * (zz * g2);
-    }
-    T* vo = a.vbar + b * 3 * g.N + q;
-    vo[0] = vb[0];
-    vo[g.N] = vb[1];
-    vo[2 * g.N] = vb[2];
   }
+  if (a.reg_lam != T(0)) {
+    T g0, g1, g2;
+    grad3(I, q, d, y, x, g, g0, g1, g2);
+    const T zz = z[q];
+    vb[0] = vb[0] - a.reg_lam * (zz * g0);
+    vb[1] = vb[1] - a.reg_lam * (zz * g1);
+    vb[2] = vb[2] - a.reg_lam * (zz * g2);
+  }
+  T* vo = a.vbar + b * 3 * g.N + q;
+  vo[0] = vb[0];
+  vo[g.N] = vb[1];
+  vo[2 * g.N] = vb[2];
 }
 
 // ------------------------------------------------------------------------------
@@ -462,46 +497,44 @@ struct VelAdj3Args {
 template <typename T, bool REG>
 __global__ void __launch_bounds__(kThreads) k_veladj_epi3d(VelAdj3Args<T> a) {
   const Grid3 g = a.g;
-  const long long total = (long long)g.B * g.N;
-  for (long long pp = blockIdx.x * (long long)kThreads + threadIdx.x; pp < total;
-       pp += (long long)gridDim.x * kThreads) {
-    const long long b = pp / g.N, q = pp - b * g.N;
-    int d, y, x;
-    coords3(q, g, d, y, x);
-    const T* __restrict__ I = a.I + b * g.N;
-    const T* __restrict__ z = a.z + b * g.N;
-    const T* __restrict__ kt = a.ktv + b * 3 * g.N;
-    T gr[3];
-    grad3(I, q, d, y, x, g, gr[0], gr[1], gr[2]);
-    const T m0 = -kt[q], m1 = -kt[g.N + q], m2 = -kt[2 * g.N + q];
-    T zb_new = a.zb[pp] + (m0 * gr[0] + m1 * gr[1] + m2 * gr[2]);
-    if (REG) {
-      const T* __restrict__ w = a.v0 + b * 3 * g.N;
-      const T km = -(w[q] * gr[0] + w[g.N + q] * gr[1] + w[2 * g.N + q] * gr[2]);
-      zb_new = zb_new + a.lam * (km + a.two_rho * z[q]);
-      a.zout[pp] = zb_new;
-      if (!isfinite(zb_new)) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
-    } else {
-      a.zb[pp] = zb_new;
-      const long long st[3] = {g.HW, (long long)g.W, 1};
-      const int pos[3] = {d, y, x};
-      const int n[3] = {g.D, g.H, g.W};
-      T acc = T(0);
+  const Vox v = vox3(g);
+  if (!v.ok) return;
+  const int d = v.d, y = v.y, x = v.x, q = v.q;
+  const long long b = v.b;
+  const long long pp = b * g.N + q;
+  const T* __restrict__ I = a.I + b * g.N;
+  const T* __restrict__ z = a.z + b * g.N;
+  const T* __restrict__ kt = a.ktv + b * 3 * g.N;
+  T gr[3];
+  grad3(I, q, d, y, x, g, gr[0], gr[1], gr[2]);
+  const T m0 = -kt[q], m1 = -kt[g.N + q], m2 = -kt[2 * g.N + q];
+  T zb_new = a.zb[pp] + (m0 * gr[0] + m1 * gr[1] + m2 * gr[2]);
+  if (REG) {
+    const T* __restrict__ w = a.v0 + b * 3 * g.N;
+    const T km = -(w[q] * gr[0] + w[g.N + q] * gr[1] + w[2 * g.N + q] * gr[2]);
+    zb_new = zb_new + a.lam * (km + a.two_rho * z[q]);
+    a.zout[pp] = zb_new;
+    if (!isfinite(zb_new)) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+  } else {
+    a.zb[pp] = zb_new;
+    const int st[3] = {(int)g.HW, g.W, 1};
+    const int pos[3] = {d, y, x};
+    const int n[3] = {g.D, g.H, g.W};
+    T acc = T(0);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const T* kc = kt + c * g.N;
-        auto qv = [&](long long qq) { return -kc[qq] * z[qq]; };
-        const int j = pos[c];
-        const T qc = qv(q);
-        const T gm = j > 0 ? qv(q - st[c]) : T(0);
-        const T gp = j < n[c] - 1 ? qv(q + st[c]) : T(0);
-        const T gf = j == 0 ? qc : (j == 1 ? gm : T(0));
-        const T gl = j == n[c] - 1 ? qc : (j == n[c] - 2 ? gp : T(0));
-        const T t = diff_adj1(gm, gp, gf, gl, j, n[c]);
-        acc = (c == 0) ? t : acc + t;
-      }
-      a.ib[pp] = a.ib[pp] + acc;
+    for (int c = 0; c < 3; ++c) {
+      const T* kc = kt + c * g.N;
+      auto qv = [&](int qq) { return -kc[qq] * z[qq]; };
+      const int j = pos[c];
+      const T qc = qv(q);
+      const T gm = j > 0 ? qv(q - st[c]) : T(0);
+      const T gp = j < n[c] - 1 ? qv(q + st[c]) : T(0);
+      const T gf = j == 0 ? qc : (j == 1 ? gm : T(0));
+      const T gl = j == n[c] - 1 ? qc : (j == n[c] - 2 ? gp : T(0));
+      const T t = diff_adj1(gm, gp, gf, gl, j, n[c]);
+      acc = (c == 0) ? t : acc + t;
     }
+    a.ib[pp] = a.ib[pp] + acc;
   }
 }
 
