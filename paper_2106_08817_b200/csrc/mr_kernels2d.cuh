@@ -986,6 +986,30 @@ __global__ void __launch_bounds__(kThreads)
   const T* tzb = tail + 3 * OXY;
   const T* t4 = tail + 4 * OXY;
   unsigned bad = 0;
+  // tile interior: every owner has both neighbours on both axes and no edge
+  // terms of the stencil transpose -> branch-free (bitwise-identical) formulas
+  const bool interior = !REG && y_org + 1 >= 2 && y_org + OY - 2 <= H - 3 && x_org + 1 >= 2 &&
+                        x_org + OX - 2 <= W - 3;
+  if (interior) {
+    for (int j = 1 + warp; j < OY - 1; j += kNW)
+      for (int i = 1 + lane; i < OX - 1; i += 32) {
+        const long long q = (long long)(y_org + j) * W + (x_org + i);
+        const int e = j * OXP + i;
+        const T g0 = (tI[e + OXP] - tI[e - OXP]) / T(2);
+        const T g1 = (tI[e + 1] - tI[e - 1]) / T(2);
+        const T m0 = -res[j * OP + i];
+        const T m1 = -res[(OY + j) * OP + i];
+        a.zb[b * N + q] = tzb[e] + (m0 * g0 + m1 * g1);
+        // G^T(mbar z): 0.5 q[j-1] - 0.5 q[j+1] per axis (fields.py:148-158)
+        const T gm = -res[(j - 1) * OP + i] * tz[e - OXP];
+        const T gp = -res[(j + 1) * OP + i] * tz[e + OXP];
+        const T hm = -res[(OY + j) * OP + i - 1] * tz[e - 1];
+        const T hp = -res[(OY + j) * OP + i + 1] * tz[e + 1];
+        const T t0 = T(0.5) * gm - T(0.5) * gp;
+        const T t1 = T(0.5) * hm - T(0.5) * hp;
+        a.ib[b * N + q] = t2[e] + (t0 + t1);
+      }
+  } else
   for (int j = 1 + warp; j < OY - 1; j += kNW)
   for (int i = 1 + lane; i < OX - 1; i += 32) {
     const int gy = y_org + j, gx = x_org + i;
