@@ -190,6 +190,8 @@ __global__ void __launch_bounds__(kThreads)
   const T* __restrict__ I = a.I + b * N;
   const T* __restrict__ z = a.z + b * N;
   const T dt = a.dt;
+  // every tile pixel at least 2 away from the image edges: central stencils only
+  const bool interior = y0 >= 2 && y0 + TY - 1 <= H - 3 && x0 >= 2 && x0 + TX - 1 <= W - 3;
 
   // corners of I or z at the foot of window pixel (r, c) (v-window coordinates)
   auto corners = [&](const T* sf, const T* __restrict__ gf, const AxisPlan<T>& py,
@@ -242,7 +244,9 @@ __global__ void __launch_bounds__(kThreads)
     if (own) corners(sz, z, py, px, za, zb2, zc, zd);
     const T ib_ = sib[vi], zb_ = szb[vi];
     T scale = T(1);
-    if (own) {
+    if (interior) {
+      scale = T(1) - dt * ((sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2));
+    } else if (own) {
       const T up = (y > 0) ? sv0[vi - VX] : vy;
       const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
       const T lf = (x > 0) ? sv1[vi - 1] : vx;
@@ -276,11 +280,17 @@ __global__ void __launch_bounds__(kThreads)
     corners(sI, I, py, px, ia, ib2, ic, id);
     corners(sz, z, py, px, za, zb2, zc, zd);
     const T ib_ = sib[vi], zb_ = szb[vi];
-    const T up = (y > 0) ? sv0[vi - VX] : vy;
-    const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
-    const T lf = (x > 0) ? sv1[vi - 1] : vx;
-    const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
-    const T wz = zb_ * (T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W)));
+    T wz;
+    if (interior) {
+      wz = zb_ * (T(1) - dt * ((sv0[vi + VX] - sv0[vi - VX]) / T(2) +
+                              (sv1[vi + 1] - sv1[vi - 1]) / T(2)));
+    } else {
+      const T up = (y > 0) ? sv0[vi - VX] : vy;
+      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+      const T lf = (x > 0) ? sv1[vi - 1] : vx;
+      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+      wz = zb_ * (T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W)));
+    }
     const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
     const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
     const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
@@ -292,13 +302,18 @@ __global__ void __launch_bounds__(kThreads)
     vb1 += -dt * dzx * wz;
     const int j = ty + 1, i = tx + 1;
     const T sm_ = s_div[(j - 1) * SX + i], sp_ = s_div[(j + 1) * SX + i];
-    const T s_first_y = (y <= 1) ? s_div[(j - y) * SX + i] : T(0);
-    const T s_last_y = (y >= H - 2) ? s_div[(j + (H - 1 - y)) * SX + i] : T(0);
-    vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
     const T sl_ = s_div[j * SX + i - 1], sr_ = s_div[j * SX + i + 1];
-    const T s_first_x = (x <= 1) ? s_div[j * SX + i - x] : T(0);
-    const T s_last_x = (x >= W - 2) ? s_div[j * SX + i + (W - 1 - x)] : T(0);
-    vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    if (interior) {  // D^T s = 0.5 s[j-1] - 0.5 s[j+1] away from the edges
+      vb0 += T(0.5) * sm_ - T(0.5) * sp_;
+      vb1 += T(0.5) * sl_ - T(0.5) * sr_;
+    } else {
+      const T s_first_y = (y <= 1) ? s_div[(j - y) * SX + i] : T(0);
+      const T s_last_y = (y >= H - 2) ? s_div[(j + (H - 1 - y)) * SX + i] : T(0);
+      vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+      const T s_first_x = (x <= 1) ? s_div[j * SX + i - x] : T(0);
+      const T s_last_x = (x >= W - 2) ? s_div[j * SX + i + (W - 1 - x)] : T(0);
+      vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    }
     const long long q = (long long)y * W + x;
     if (a.reg_lam != T(0)) {  // k = 0: fold -lam*m0
       const int ce = (ty + HB) * GX + tx + HB;
