@@ -409,9 +409,11 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
     return check_cuda("memset flags");
   rc = launch_cost_terms2d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
   if (rc) return check_rc(rc, "cost_terms");
+  // zbar_T = 0 and the first scatter targets; afterwards the velocity-adjoint
+  // kernel of each step zeroes the buffers the next step scatters into
   if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
+  if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
   for (int step = T_ - 1; step >= 0; --step) {
-    if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
     rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
                                 cur + S1, acc, acc + S1, vbar, s, step == 0 ? lam : 0.0);
     if (rc) return check_rc(rc, "sl_adjoint");
@@ -425,6 +427,10 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
     a.lam = (T)lam;
     a.two_rho = (T)(2.0 * rho);
     const bool reg = (step == 0);
+    if (!reg) {  // ibar/zbar of step k+1 are consumed: zero them for the next scatter
+      a.zero_a = cur;
+      a.zero_b = cur + S1;
+    }
     if (reg) {
       a.v0 = v;  // v at k = 0
       a.zout = static_cast<T*>(zbar0);

@@ -69,7 +69,8 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
 template <typename T, int R, bool REG>
 int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
   // Measured on B200 (cfg2): 0.41 ms vs 0.38 ms for the tile kernel, which
-  // overlaps all epilogue operand loads with pass 2.  Kept for future tuning.
+  // overlaps all epilogue operand loads with pass 2.  Kept for future tuning
+  // (enabling it also requires the zero_a/zero_b accumulator zeroing).
   constexpr bool kEnabled = false;
   if constexpr (sizeof(T) != 4 || !kEnabled) {
     return 1;

@@ -856,6 +856,8 @@ struct VelAdjArgs {
   int32_t* flags;  // per pair non-finite flag
   T lam, two_rho;
   int use_tma;
+  T* zero_a;       // nullable: buffers zeroed at the owner pixels (the consumed
+  T* zero_b;       //   ibar/zbar of step k+1 = next step's scatter targets)
   Grid2 g;
 };
 
@@ -1000,6 +1002,10 @@ __global__ void __launch_bounds__(kThreads)
         const T m0 = -res[j * OP + i];
         const T m1 = -res[(OY + j) * OP + i];
         a.zb[b * N + q] = tzb[e] + (m0 * g0 + m1 * g1);
+        if (a.zero_a) {
+          a.zero_a[b * N + q] = T(0);
+          a.zero_b[b * N + q] = T(0);
+        }
         // G^T(mbar z): 0.5 q[j-1] - 0.5 q[j+1] per axis (fields.py:148-158)
         const T gm = -res[(j - 1) * OP + i] * tz[e - OXP];
         const T gp = -res[(j + 1) * OP + i] * tz[e + OXP];
@@ -1030,6 +1036,10 @@ __global__ void __launch_bounds__(kThreads)
       bad |= isfinite(zb_new) ? 0u : 1u;
     } else {
       a.zb[b * N + q] = zb_new;
+      if (a.zero_a) {
+        a.zero_a[b * N + q] = T(0);
+        a.zero_b[b * N + q] = T(0);
+      }
       // ib += G^T(mbar z) (objective.py:160-161), gather form on q_c = mbar_c * z
       auto q0 = [&](int jr) { return -res[jr * OP + i] * tz[jr * OXP + i]; };
       auto q1 = [&](int ic) { return -res[(OY + j) * OP + ic] * tz[j * OXP + ic]; };
