@@ -31,7 +31,9 @@ struct StreamCfg {
   static constexpr int PXZ = round_up(RX + A - 1, A);      // z box width
   static constexpr int PP = (RX % 2) ? RX : RX + 1;        // product pitch (odd)
   static constexpr int RING = G + 2 * R;  // filtered rows kept
-  static constexpr int RP = OX + 2;       // ring pitch (even: 8-byte column pairs)
+  static constexpr int RP = OX + 4;       // ring pitch: 16-B rows (float4 stores/copies),
+                                          // 8-byte column pairs; 68 = 4 mod 32 keeps the
+                                          // quarter-warp float4 stores conflict-free
   // smem layout (elements after the 128-B head)
   static constexpr int o_ist = 0;
   static constexpr int n_ist = round_up((G + 2) * PXI + A, 32);
@@ -170,13 +172,14 @@ __global__ void __launch_bounds__(kThreads)
               if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
             }
           }
-          T* d0 = ring + c * RING * RP + (u0 + r - ring_lo) * RP + ib * kRB;
-#pragma unroll
-          for (int o = 0; o < kRB; ++o) d0[o] = acc[o].x;
+          float4* d0 = reinterpret_cast<float4*>(ring + c * RING * RP + (u0 + r - ring_lo) * RP +
+                                                 ib * kRB);
+          d0[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+          d0[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
           if (r + 16 < cin) {
-            T* d1 = d0 + 16 * RP;
-#pragma unroll
-            for (int o = 0; o < kRB; ++o) d1[o] = acc[o].y;
+            float4* d1 = d0 + 16 * RP / 4;
+            d1[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+            d1[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
           }
         }
         __syncthreads();
@@ -231,18 +234,22 @@ __global__ void __launch_bounds__(kThreads)
       }
       const int gx = x0 + i;
       T* vo = (c == 0 ? v0 : v1) + gx;
+      const bool pair_ok = gx + 1 < W && ((W & 1) == 0);  // 8-byte aligned float2 store
 #pragma unroll
       for (int o = 0; o < kRB; ++o) {
         const int gy = y0 + jb * kRB + o;
         if (gy < H) {
           const T a0 = -acc[o].x, a1 = -acc[o].y;
-          if (gx < W) {
-            vo[(long long)gy * W] = a0;
-            flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
+          if (pair_ok) {
+            *reinterpret_cast<float2*>(vo + (long long)gy * W) = make_float2(a0, a1);
+          } else {
+            if (gx < W) vo[(long long)gy * W] = a0;
+            if (gx + 1 < W) vo[(long long)gy * W + 1] = a1;
           }
-          if (gx + 1 < W) {
-            vo[(long long)gy * W + 1] = a1;
-            flags |= guard_bits(a1, MR_GUARD_VELOCITY_NONFINITE);
+          // one compare on the common path; exact guard bits only when it fails
+          if (!(fabsf(a0) <= 1e6f && fabsf(a1) <= 1e6f)) {
+            if (gx < W) flags |= guard_bits(a0, MR_GUARD_VELOCITY_NONFINITE);
+            if (gx + 1 < W) flags |= guard_bits(a1, MR_GUARD_VELOCITY_NONFINITE);
           }
         }
       }
@@ -253,11 +260,14 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int band = 0; band < 2 * R; band += G) {
       const int nrow = (2 * R - band) < G ? (2 * R - band) : G;  // compile-time per band
-      for (int rr = band + warp; rr < band + nrow; rr += kNW)
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          for (int i = lane; i < OX; i += 32)
-            ring[c * RING * RP + rr * RP + i] = ring[c * RING * RP + (rr + G) * RP + i];
+      // float4 copy: each warp moves two rows (16 float4 per row and component)
+      for (int t = warp * 32 + lane; t < nrow * 2 * (OX / 4); t += kThreads) {
+        const int q4 = t % (OX / 4), rest = t / (OX / 4);
+        const int c = rest & 1, rr = band + (rest >> 1);
+        float4* dst = reinterpret_cast<float4*>(ring + c * RING * RP + rr * RP) + q4;
+        const float4* src = reinterpret_cast<const float4*>(ring + c * RING * RP + (rr + G) * RP) + q4;
+        *dst = *src;
+      }
       __syncthreads();
     }
     ring_lo = y0 + G - R;
