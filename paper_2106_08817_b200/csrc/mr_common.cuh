@@ -78,19 +78,17 @@ __device__ __forceinline__ AxisPlan<T> plan_axis(int pos, T vel, T dt, int n);
 template <>
 __device__ __forceinline__ AxisPlan<float> plan_axis<float>(int pos, float vel, float dt, int n) {
   AxisPlan<float> p;
-  float d = -(dt * vel);
-  float fl = floorf(d);
-  float fr = d - fl;
-  // bound before the int conversion (huge values only occur after the guard fired)
-  fl = fminf(fmaxf(fl, -4.0f * n - 4.0f), 4.0f * n + 4.0f);
-  int ii = pos + (int)fl;
-  if (ii < 0 || (ii == 0 && fr == 0.0f)) {
-    p.i0 = 0; p.f = 0.0f; p.inside = false;
-  } else if (ii >= n - 1) {
-    p.i0 = n - 2; p.f = 1.0f; p.inside = false;
-  } else {
-    p.i0 = ii; p.f = fr; p.inside = true;
-  }
+  const float d = -(dt * vel);
+  // floor as a saturating int conversion; bounded so pos + fl cannot overflow
+  // (huge displacements only occur after the guard fired)
+  const int fl = min(max(__float2int_rd(d), -(1 << 24)), 1 << 24);
+  const float fr = d - (float)fl;
+  const int ii = pos + fl;
+  const bool lo = ii < 0 || (ii == 0 && fr == 0.0f);
+  const bool hi = ii >= n - 1;
+  p.i0 = lo ? 0 : (hi ? n - 2 : ii);
+  p.f = lo ? 0.0f : (hi ? 1.0f : fr);
+  p.inside = !(lo || hi);
   return p;
 }
 

@@ -146,6 +146,30 @@ struct AdjCfg {
   static constexpr size_t bytes = C::head + sizeof(T) * (size_t)(2 * nG + 4 * nV + nS);
 };
 
+// 32-bit-key variant of scatter4_merged (cell index within one pair < 2^31)
+template <typename T>
+__device__ __forceinline__ void scatter4_merged32(T* __restrict__ out, int cell, bool valid, int W,
+                                                  T ca, T cb, T cc, T cd) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? cell : -4;
+  const int prev_key = __shfl_up_sync(full, key, 1);
+  const int next_key = __shfl_down_sync(full, key, 1);
+  const T pc = __shfl_up_sync(full, cc, 1);
+  const T pd = __shfl_up_sync(full, cd, 1);
+  if (!valid) return;
+  if (lane > 0 && prev_key >= 0 && prev_key + 1 == key) {
+    ca += pc;
+    cb += pd;
+  }
+  atomicAdd(out + cell, ca);
+  atomicAdd(out + cell + W, cb);
+  if (!(lane < 31 && next_key >= 0 && key + 1 == next_key)) {
+    atomicAdd(out + cell + 1, cc);
+    atomicAdd(out + cell + W + 1, cd);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     k_sl_adjoint2d_tma(AdjArgs<T> a, const __grid_constant__ AdjMaps maps) {
@@ -256,11 +280,10 @@ __global__ void __launch_bounds__(kThreads)
     s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * bilerp(za, zb2, zc, zd, py.f, px.f)) : T(0);
     const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
     const T wz = zb_ * scale;
-    const long long c00 = (long long)py.i0 * W + px.i0;
-    scatter4_merged(ibo, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
-                    fy * fx * ib_);
-    scatter4_merged(zbo, c00, own, (long long)W, wy * wx * wz, fy * wx * wz, wy * fx * wz,
-                    fy * fx * wz);
+    const int c00 = py.i0 * W + px.i0;
+    scatter4_merged32(ibo, c00, own, W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
+                      fy * fx * ib_);
+    scatter4_merged32(zbo, c00, own, W, wy * wx * wz, fy * wx * wz, wy * fx * wz, fy * fx * wz);
     if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
   }
   __syncthreads();
