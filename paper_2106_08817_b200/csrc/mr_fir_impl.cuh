@@ -20,8 +20,9 @@ int velocity_stream_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStrea
   } else {
   using C = StreamCfg<T, R>;
   if (C::bytes > 227 * 1024) return 1;
-  // one CTA per strip walks all rows: only worth it with >= 2 strips per SM
-  if ((long long)((g.W + C::OX - 1) / C::OX) * g.B < 2LL * 148) return 1;
+  // one CTA per strip walks all rows: only worth it with ~1 strip per SM or more
+  // (the host pipeline runs 4 groups of pairs concurrently, 128 strips each at cfg2)
+  if ((long long)((g.W + C::OX - 1) / C::OX) * g.B < 128) return 1;
   CUtensorMap mI, mZ;
   if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, C::PXI, C::G + 2) ||
       !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, C::PXZ, C::G))
@@ -195,14 +196,25 @@ int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D
 
 }  // namespace mr
 
-#define MR_INSTANTIATE_FIR(T)                                                                   \
+// One launcher per translation unit (mr_fir_<launcher>_<precision>.cu) so the
+// heavily unrolled radius instantiations compile in parallel.
+#define MR_INSTANTIATE_VELOCITY(T)                                                              \
   namespace mr {                                                                                \
   template int launch_velocity2d<T>(const Grid2&, int, const Taps<T>&, const T*, const T*, T*,  \
                                     int32_t*, int, cudaStream_t);                               \
+  }
+#define MR_INSTANTIATE_SMOOTH(T)                                                                \
+  namespace mr {                                                                                \
   template int launch_smooth2d<T>(const Grid2&, int, const Taps<T>&, const T*, T*, bool,        \
                                   cudaStream_t);                                                \
+  }
+#define MR_INSTANTIATE_VELADJ(T)                                                                \
+  namespace mr {                                                                                \
   template int launch_velocity_adj2d<T>(const Grid2&, int, const Taps<T>&,                      \
                                         const VelAdjArgs<T>&, bool, cudaStream_t);              \
+  }
+#define MR_INSTANTIATE_AXIS0(T)                                                                 \
+  namespace mr {                                                                                \
   template int launch_fir_axis0<T>(int, const Taps<T>&, const T*, T*, int, int, long long, bool, \
                                    int, int32_t*, int, cudaStream_t);                           \
   }

@@ -1,0 +1,2 @@
+#include "mr_fir_impl.cuh"
+MR_INSTANTIATE_SMOOTH(float)

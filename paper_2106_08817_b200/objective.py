@@ -126,8 +126,17 @@ class ShootingCost(torch.autograd.Function):
 
 
 def cost_and_grad_batch(source: torch.Tensor, target: torch.Tensor, z0: torch.Tensor,
-                        cfg: ShootingConfig, lam: float, rho: float, raise_on_divergence=True):
-    """One grad() per pair of a device batch -> (zbar [B,*shape], terms [B,4] fp64, guard [B,T+1])."""
+                        cfg: ShootingConfig, lam: float, rho: float, raise_on_divergence=True,
+                        chunks: int | None = None):
+    """One grad() per pair of a batch -> (zbar [B,*shape], terms [B,4] fp64, guard [B,T+1]).
+
+    Device tensors in -> device tensors out, stream-ordered on the current stream.
+    Host tensors in -> host tensors out: the batch is pipelined in ``chunks``
+    groups of pairs (see :func:`_host_pipeline`), so the host<->device copies
+    overlap the shooting of the other groups.
+    """
+    if not z0.is_cuda:
+        return _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunks)
     _require_sl(cfg)
     B = z0.shape[0]
     shape = tuple(z0.shape[1:])
@@ -139,3 +148,90 @@ def cost_and_grad_batch(source: torch.Tensor, target: torch.Tensor, z0: torch.Te
     if raise_on_divergence:
         engine.raise_on_guard(traj)
     return bufs.zbar, bufs.terms, traj.guard
+
+
+_PIPE_STREAMS: dict = {}
+
+
+def _pipe_streams(device, n: int):
+    """Persistent streams of the host pipeline (one upload stream + n pair groups), so
+    the caching allocator reuses each group's trajectory across calls."""
+    key = (device.index, n)
+    if key not in _PIPE_STREAMS:
+        _PIPE_STREAMS[key] = (torch.cuda.Stream(device), [torch.cuda.Stream(device) for _ in range(n)])
+    return _PIPE_STREAMS[key]
+
+
+def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunks):
+    """Host-buffer grad() of a batch with the PCIe transfers hidden behind compute.
+
+    The pairs are split into ``chunks`` groups, each with its own trajectory and
+    stream.  One upload stream copies every group's (I0, z0) first, then every
+    group's target J (needed only by the adjoint, after the forward sweep).  Group
+    g's forward waits for its (I0, z0) event, its adjoint for its J event, and its
+    dH/dz0, cost rows and guard go back to pinned host memory on its own stream
+    while the other groups still compute.  The groups' kernels run concurrently,
+    so the device sees the whole batch; per pair the result is the same as a
+    device-tensor call.
+    """
+    _require_sl(cfg)
+    B = z0.shape[0]
+    shape = tuple(z0.shape[1:])
+    if tuple(source.shape) != tuple(z0.shape) or tuple(target.shape) != tuple(z0.shape):
+        raise FieldError("source/target/z0 batch shapes differ")
+    if chunks is None:
+        chunks = 4 if B >= 16 else (2 if B >= 2 else 1)
+    chunks = max(1, min(int(chunks), B))
+    dtype = cfg.dtype if z0.dtype not in (torch.float32, torch.float64) else z0.dtype
+    device = torch.device("cuda", torch.cuda.current_device())
+
+    def pinned(t):
+        t = t.to(dtype).contiguous()
+        return t if t.is_pinned() else t.pin_memory()
+
+    src_h, tgt_h, z0_h = pinned(source), pinned(target), pinned(z0)
+    zbar_h = torch.empty((B,) + shape, dtype=dtype, pin_memory=True)
+    terms_h = torch.empty((B, 4), dtype=torch.float64, pin_memory=True)
+    guard_h = torch.empty((B, cfg.n_steps + 1), dtype=torch.int32, pin_memory=True)
+    up, streams = _pipe_streams(device, chunks)
+    up.wait_stream(torch.cuda.current_stream(device))
+    bounds = [(B * g // chunks, B * (g + 1) // chunks) for g in range(chunks)]
+
+    trajs, tgts, ev_in, ev_J = [], [], [], []
+    for g, (a, b) in enumerate(bounds):
+        with torch.cuda.stream(streams[g]):
+            trajs.append(engine.allocate_trajectory(b - a, shape, cfg.n_steps, dtype, device))
+            tgts.append(torch.empty((b - a,) + shape, dtype=dtype, device=device))
+    with torch.cuda.stream(up):
+        for g, (a, b) in enumerate(bounds):
+            trajs[g].I[0].copy_(src_h[a:b], non_blocking=True)
+            trajs[g].z[0].copy_(z0_h[a:b], non_blocking=True)
+            ev_in.append(up.record_event())
+        for g, (a, b) in enumerate(bounds):
+            tgts[g].copy_(tgt_h[a:b], non_blocking=True)
+            ev_J.append(up.record_event())
+    w = cfg.kernel.weights
+    keep = []
+    for g, (a, b) in enumerate(bounds):
+        s = streams[g]
+        with torch.cuda.stream(s):  # every allocation and launch of group g is on s
+            s.wait_event(ev_in[g])
+            engine.shoot_forward(trajs[g], cfg.mu, w, stream=s)
+            s.wait_event(ev_J[g])
+            bufs = engine.shoot_adjoint(trajs[g], tgts[g], lam, rho, cfg.mu, w, stream=s)
+            keep.append(bufs)
+            zbar_h[a:b].copy_(bufs.zbar, non_blocking=True)
+            terms_h[a:b].copy_(bufs.terms, non_blocking=True)
+            guard_h[a:b].copy_(trajs[g].guard, non_blocking=True)
+            # the upload stream wrote into this group's buffers
+            for t in (trajs[g].I, trajs[g].z, tgts[g]):
+                t.record_stream(up)
+    for s in streams:
+        s.synchronize()
+    if raise_on_divergence:
+        rep = engine.guard_report(guard_h)
+        if rep is not None:
+            from .errors import IntegrationDiverged
+
+            raise IntegrationDiverged(rep[1], rep[2])
+    return zbar_h, terms_h, guard_h
