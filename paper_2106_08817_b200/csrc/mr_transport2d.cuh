@@ -250,11 +250,13 @@ __global__ void __launch_bounds__(kThreads)
     s_div[j * SX + i] = sv;
   }
 
-  // ---- phase 1: owners' s and the scatters (warp-merged, lanes = consecutive x) ----
+  // ---- phase 1: per owner pixel the plans, corners, scatters, s, and the partial
+  //      vbar (coordinate-gradient terms) kept in registers for phase 2 ----
   T* __restrict__ ibo = a.ib + b * N;
   T* __restrict__ zbo = a.zb + b * N;
   constexpr int CPR = TX / 32;
-#pragma unroll 1
+  T vbp0[C::PIX], vbp1[C::PIX];
+#pragma unroll
   for (int k = 0; k < C::PIX; ++k) {
     const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
     const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
@@ -264,8 +266,12 @@ __global__ void __launch_bounds__(kThreads)
     const T vy = sv0[vi], vx = sv1[vi];
     const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
     const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
+    T ia = T(0), ib2 = T(0), ic = T(0), id = T(0);
     T za = T(0), zb2 = T(0), zc = T(0), zd = T(0);
-    if (own) corners(sz, z, py, px, za, zb2, zc, zd);
+    if (own) {
+      corners(sz, z, py, px, za, zb2, zc, zd);
+      corners(sI, I, py, px, ia, ib2, ic, id);
+    }
     const T ib_ = sib[vi], zb_ = szb[vi];
     T scale = T(1);
     if (interior) {
@@ -277,52 +283,32 @@ __global__ void __launch_bounds__(kThreads)
       const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
       scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
     }
-    s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * bilerp(za, zb2, zc, zd, py.f, px.f)) : T(0);
     const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
+    s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * (wy * wx * za + fy * wx * zb2 + wy * fx * zc + fy * fx * zd)) : T(0);
     const T wz = zb_ * scale;
     const int c00 = py.i0 * W + px.i0;
     scatter4_merged32(ibo, c00, own, W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
                       fy * fx * ib_);
     scatter4_merged32(zbo, c00, own, W, wy * wx * wz, fy * wx * wz, wy * fx * wz, fy * fx * wz);
     if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
+    // vbar = -dt (d/dy, d/dx)[P I] ibar - dt (d/dy, d/dx)[P z] w  (objective.py:131-132,143-145)
+    const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
+    const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
+    const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
+    const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
+    vbp0[k] = -dt * ddy * ib_ + -dt * dzy * wz;
+    vbp1[k] = -dt * ddx * ib_ + -dt * dzx * wz;
   }
   __syncthreads();
 
-  // ---- phase 2: vbar (objective.py:131-132, 143-147) ----
-#pragma unroll 1
+  // ---- phase 2: vbar += D^T s (objective.py:146-147), then the k = 0 fold ----
+#pragma unroll
   for (int k = 0; k < C::PIX; ++k) {
     const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
     const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
     const int x = x0 + tx, y = y0 + ty;
     if (x >= W || y >= H) continue;
-    const int vi = (ty + 1) * VX + tx + 1;
-    const T vy = sv0[vi], vx = sv1[vi];
-    const AxisPlan<T> py = plan_axis<T>(y, vy, dt, H);
-    const AxisPlan<T> px = plan_axis<T>(x, vx, dt, W);
-    T ia, ib2, ic, id, za, zb2, zc, zd;
-    corners(sI, I, py, px, ia, ib2, ic, id);
-    corners(sz, z, py, px, za, zb2, zc, zd);
-    const T ib_ = sib[vi], zb_ = szb[vi];
-    T wz;
-    if (interior) {
-      wz = zb_ * (T(1) - dt * ((sv0[vi + VX] - sv0[vi - VX]) / T(2) +
-                              (sv1[vi + 1] - sv1[vi - 1]) / T(2)));
-    } else {
-      const T up = (y > 0) ? sv0[vi - VX] : vy;
-      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
-      const T lf = (x > 0) ? sv1[vi - 1] : vx;
-      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
-      wz = zb_ * (T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W)));
-    }
-    const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
-    const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
-    const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
-    T vb0 = -dt * ddy * ib_;
-    T vb1 = -dt * ddx * ib_;
-    const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
-    const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
-    vb0 += -dt * dzy * wz;
-    vb1 += -dt * dzx * wz;
+    T vb0 = vbp0[k], vb1 = vbp1[k];
     const int j = ty + 1, i = tx + 1;
     const T sm_ = s_div[(j - 1) * SX + i], sp_ = s_div[(j + 1) * SX + i];
     const T sl_ = s_div[j * SX + i - 1], sr_ = s_div[j * SX + i + 1];
