@@ -69,9 +69,10 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
 
 template <typename T, int R, bool REG>
 int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
-  // Measured on B200 (cfg2): 0.41 ms vs 0.38 ms for the tile kernel, which
-  // overlaps all epilogue operand loads with pass 2.  Kept for future tuning
-  // (enabling it also requires the zero_a/zero_b accumulator zeroing).
+  // FIR work 2*(2R+1) FFMA per computed output (no y halo), 62/64 x 30/32 owners.
+  // Measured on B200 (cfg2, FFMA2 passes, interior epilogue): 0.331 ms against
+  // 0.294 ms for the tile kernel (exposed vbar TMA at each block start: the
+  // staging buffer doubles as the epilogue's I/z tile).  Kept for tuning.
   constexpr bool kEnabled = false;
   if constexpr (sizeof(T) != 4 || !kEnabled) {
     return 1;
@@ -79,6 +80,7 @@ int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStre
     using C = StreamAdjCfg<T, R>;
     constexpr size_t bytes = REG ? C::bytes_reg : C::bytes_noreg;
     if (bytes > 227 * 1024) return 1;
+    if ((long long)((g.W + C::OX - 3) / (C::OX - 2)) * g.B < 128) return 1;
     VelAdjMaps m;
     const long long B2 = 2LL * g.B;
     const bool ok = make_map3<T>(&m.vbar, a.vbar, g.W, g.H, B2, C::PXZ, C::G) &&
@@ -218,3 +220,27 @@ int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D
   template int launch_fir_axis0<T>(int, const Taps<T>&, const T*, T*, int, int, long long, bool, \
                                    int, int32_t*, int, cudaStream_t);                           \
   }
+
+// Radius groups: the per-radius kernels of the two heavy launchers (velocity,
+// velocity adjoint) are instantiated in mr_fir_<launcher>_<prec>_g<k>.cu (radius
+// r with r % 4 == k) so they compile in parallel; the dispatching translation unit
+// sees them as extern templates.
+#define MR_RADIUS_GROUP0(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+#define MR_RADIUS_GROUP1(X) X(1) X(5) X(9) X(13) X(17) X(21) X(25) X(29)
+#define MR_RADIUS_GROUP2(X) X(2) X(6) X(10) X(14) X(18) X(22) X(26) X(30)
+#define MR_RADIUS_GROUP3(X) X(3) X(7) X(11) X(15) X(19) X(23) X(27) X(31)
+#define MR_VELOCITY_R_DECL(PFX, T, RR) \
+  PFX template int velocity_r<T, RR>(const Grid2&, const Taps<T>&, VelArgs<T>, cudaStream_t);
+#define MR_VELADJ_R_DECL(PFX, T, RR)                                                           \
+  PFX template int veladj_r<T, RR, true>(const Grid2&, const Taps<T>&, VelAdjArgs<T>,           \
+                                         cudaStream_t);                                         \
+  PFX template int veladj_r<T, RR, false>(const Grid2&, const Taps<T>&, VelAdjArgs<T>,          \
+                                          cudaStream_t);
+#define MR_VEL_EXTERN_F32(RR) MR_VELOCITY_R_DECL(extern, float, RR)
+#define MR_VEL_EXTERN_F64(RR) MR_VELOCITY_R_DECL(extern, double, RR)
+#define MR_VEL_INST_F32(RR) MR_VELOCITY_R_DECL(, float, RR)
+#define MR_VEL_INST_F64(RR) MR_VELOCITY_R_DECL(, double, RR)
+#define MR_VADJ_EXTERN_F32(RR) MR_VELADJ_R_DECL(extern, float, RR)
+#define MR_VADJ_EXTERN_F64(RR) MR_VELADJ_R_DECL(extern, double, RR)
+#define MR_VADJ_INST_F32(RR) MR_VELADJ_R_DECL(, float, RR)
+#define MR_VADJ_INST_F64(RR) MR_VELADJ_R_DECL(, double, RR)

@@ -1,2 +1,5 @@
 #include "mr_fir_impl.cuh"
+namespace mr {
+MR_RADIUS_LIST(MR_VADJ_EXTERN_F32)
+}
 MR_INSTANTIATE_VELADJ(float)

@@ -1,0 +1,4 @@
+#include "mr_fir_impl.cuh"
+namespace mr {
+MR_RADIUS_GROUP1(MR_VADJ_INST_F32)
+}

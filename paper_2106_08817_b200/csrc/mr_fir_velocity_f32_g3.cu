@@ -1,0 +1,4 @@
+#include "mr_fir_impl.cuh"
+namespace mr {
+MR_RADIUS_GROUP3(MR_VEL_INST_F32)
+}

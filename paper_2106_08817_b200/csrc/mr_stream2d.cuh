@@ -115,10 +115,11 @@ __global__ void __launch_bounds__(kThreads)
           const bool yin = u > 0 && u < H - 1;  // warp-uniform
           if (yin && x_interior) {              // branch-free central differences
             for (int i = i_lo + lane; i < i_hi; i += 32) {
+              // z * ((a - b) / 2) == (z / 2) * (a - b) exactly (halving is exact)
               const T* c = crow + i;
-              const T zz = zrow[i];
-              p0[i] = zz * ((c[PXI] - c[-PXI]) / T(2));
-              p1[i] = zz * ((c[1] - c[-1]) / T(2));
+              const T hz = T(0.5) * zrow[i];
+              p0[i] = hz * (c[PXI] - c[-PXI]);
+              p1[i] = hz * (c[1] - c[-1]);
             }
           } else {
             for (int i = i_lo + lane; i < i_hi; i += 32) {
@@ -235,6 +236,25 @@ __global__ void __launch_bounds__(kThreads)
       const int gx = x0 + i;
       T* vo = (c == 0 ? v0 : v1) + gx;
       const bool pair_ok = gx + 1 < W && ((W & 1) == 0);  // 8-byte aligned float2 store
+      const int gyb = y0 + jb * kRB;
+      if (pair_ok && gyb + kRB <= H) {  // whole block in the image: plain float2 stores
+        float2* vrow = reinterpret_cast<float2*>(vo + gyb * W);  // < N per component
+        bool big = false;
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+          const float2 val = make_float2(-acc[o].x, -acc[o].y);
+          vrow[o * (W / 2)] = val;
+          big |= !(fabsf(val.x) <= 1e6f && fabsf(val.y) <= 1e6f);
+        }
+        if (big) {  // exact guard bits only when a value failed the one-compare test
+#pragma unroll
+          for (int o = 0; o < kRB; ++o) {
+            flags |= guard_bits(-acc[o].x, MR_GUARD_VELOCITY_NONFINITE);
+            flags |= guard_bits(-acc[o].y, MR_GUARD_VELOCITY_NONFINITE);
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int o = 0; o < kRB; ++o) {
         const int gy = y0 + jb * kRB + o;
@@ -300,13 +320,13 @@ struct StreamAdjCfg {
   static constexpr int PXZ = round_up(RX + A - 1, A);  // vbar box width
   static constexpr int PP = (RX % 2) ? RX : RX + 1;
   static constexpr int RING = G + 2 * R;
-  static constexpr int RP = OX + 1;
+  static constexpr int RP = OX + 4;  // 16-B rows: float4 ring stores / copies, float2 column pairs
   static constexpr int OXP = OX + A;                   // epilogue box width
   static constexpr int EPL = round_up(G * OXP, 32);    // one epilogue operand (I or z)
   static constexpr int o_st = 0;  // vbar staging [2][G][PXZ]; after a block's last group: I, z
   static constexpr int n_st1 = round_up(G * PXZ + A, 32);
   static constexpr int o_p = o_st + 2 * n_st1;         // P [2][G][PP]; later res [2][G][RP]
-  static constexpr int n_p = round_up(2 * G * PP, 32);
+  static constexpr int n_p = round_up(2 * G * (PP > RP ? PP : RP), 32);
   static constexpr int o_ring = o_p + n_p;
   static constexpr int n_ring = round_up(2 * RING * RP, 32);
   static constexpr size_t head = 128;
@@ -383,58 +403,79 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
       mbar_wait(bar, ph0);
       ph0 ^= 1u;
       // vbar rows -> odd-pitch P (zeros outside the image came from the TMA fill)
-      for (int r = warp; r < cin; r += NW)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const T* srow = st0 + c * C::n_st1 + offV + r * PXZ;
-          T* prow = P + c * G * PP + r * PP;
-          for (int i = lane; i < RX; i += 32) prow[i] = srow[i];
+      // (16-B loads of the aligned staged row, scalar stores to the shifted odd-pitch row)
+      static_assert(PXZ % 4 == 0, "staged rows are 16-B aligned");
+      for (int rc = warp; rc < 2 * cin; rc += NW) {
+        const int r = rc >> 1, c = rc & 1;
+        const float4* srow = reinterpret_cast<const float4*>(st0 + c * C::n_st1 + r * PXZ);
+        T* prow = P + c * G * PP + r * PP - offV;  // staged element i -> prow[i]
+        for (int q4 = lane; q4 < PXZ / 4; q4 += 32) {
+          const float4 v4 = srow[q4];
+          const int i = 4 * q4;
+          if (i >= offV && i < offV + RX) prow[i] = v4.x;
+          if (i + 1 >= offV && i + 1 < offV + RX) prow[i + 1] = v4.y;
+          if (i + 2 >= offV && i + 2 < offV + RX) prow[i + 2] = v4.z;
+          if (i + 3 >= offV && i + 3 < offV + RX) prow[i + 3] = v4.w;
         }
+      }
       __syncthreads();
       const int nu = u0 + cnt;
       if (tid == 0 && nu < H && nu < need_hi) {  // next group of this block
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         issue_v(nu);
       }
-      // horizontal transposed FIR of the new rows -> ring (lanes <-> rows)
+      // horizontal transposed FIR of the new rows -> ring: rows (r, r+16) per thread (FFMA2)
       constexpr int NB = OX / kRB;
-      for (int cb = warp; cb < 2 * NB; cb += NW) {
-        const int r = lane;
-        if (r >= cin) continue;
-        const int ib = cb % NB, c = cb / NB;
-        const T* src = P + c * G * PP + r * PP + ib * kRB;
-        T acc[kRB];
+      static_assert(NB % 2 == 0 && 2 * (NB / 2) == NW, "one (component, column-block pair) per warp");
+      {
+        const int cb = warp;
+        const int r = lane & 15;
+        const int ib = 2 * (cb % (NB / 2)) + (lane >> 4);
+        const int c = cb / (NB / 2);
+        if (r < cin) {
+          const T* s0 = P + c * G * PP + r * PP + ib * kRB;
+          const T* s1 = s0 + 16 * PP;
+          float2 acc[kRB];
 #pragma unroll
-        for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+          for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < kRB + 2 * R; ++t) {
-          const T x = src[t];
+          for (int t = 0; t < kRB + 2 * R; ++t) {
+            const float2 x = make_float2(s0[t], s1[t]);
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) {
-            const int tap = t - o;
-            if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+            for (int o = 0; o < kRB; ++o) {
+              const int tap = t - o;
+              if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
+            }
+          }
+          const int gx0 = x_org + ib * kRB;
+          if (gx0 <= 0 && gx0 + kRB > 0) {  // column 0: sum_{d=0..R} W[R-d] g[d]
+            const int o = -gx0;
+            float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = 0; d <= R; ++d)
+              s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R - d], s2);
+#pragma unroll
+            for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+          }
+          if (gx0 <= W - 1 && gx0 + kRB > W - 1) {  // column n-1
+            const int o = W - 1 - gx0;
+            float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = -R; d <= 0; ++d)
+              s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R + d], s2);
+#pragma unroll
+            for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+          }
+          float4* d0 = reinterpret_cast<float4*>(ring + c * RING * RP + (u0 + r - ring_lo) * RP +
+                                                 ib * kRB);
+          d0[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+          d0[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
+          if (r + 16 < cin) {
+            float4* d1 = d0 + 16 * RP / 4;
+            d1[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+            d1[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
           }
         }
-        const int gx0 = x_org + ib * kRB;
-        if (gx0 <= 0 && gx0 + kRB > 0) {  // column 0: sum_{d=0..R} W[R-d] g[d]
-          const int o = -gx0;
-          T s = T(0);
-#pragma unroll
-          for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[o + R + d], s);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-        }
-        if (gx0 <= W - 1 && gx0 + kRB > W - 1) {  // column n-1
-          const int o = W - 1 - gx0;
-          T s = T(0);
-#pragma unroll
-          for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[o + R + d], s);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-        }
-        T* dst = ring + c * RING * RP + (u0 + r - ring_lo) * RP + ib * kRB;
-#pragma unroll
-        for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
       }
       __syncthreads();
       next_u = u0 + cin;
@@ -449,6 +490,8 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
     // ---- owner operands of the epilogue into registers (in flight during the pass) ----
     constexpr int NJ = (G - 2 + NW - 1) / NW, NI = (OX - 2 + 31) / 32;
     T pre_a[NJ][NI], pre_b[NJ][NI], pre_c[NJ][NI];
+    const T* __restrict__ zb_p = a.zb + b * N;
+    const T* __restrict__ o2_p = REG ? a.v0 + b * 2 * N : a.ib + b * N;
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
@@ -456,59 +499,54 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
         const int j = 1 + warp + jj * NW, i = 1 + lane + ii * 32;
         const int gy = yc0 + j, gx = x_org + i;
         const bool ok = j < G - 1 && i < OX - 1 && gy < H && gx < W;
-        const long long q = ok ? (long long)gy * W + gx : 0;
-        pre_a[jj][ii] = ok ? a.zb[b * N + q] : T(0);
-        if (REG) {
-          const T* __restrict__ w0 = a.v0 + b * 2 * N;
-          pre_b[jj][ii] = ok ? w0[q] : T(0);
-          pre_c[jj][ii] = ok ? w0[N + q] : T(0);
-        } else {
-          pre_b[jj][ii] = ok ? a.ib[b * N + q] : T(0);
-          pre_c[jj][ii] = T(0);
-        }
+        const int q = ok ? gy * W + gx : 0;  // < N < 2^31 per pair
+        pre_a[jj][ii] = ok ? zb_p[q] : T(0);
+        pre_b[jj][ii] = ok ? o2_p[q] : T(0);
+        pre_c[jj][ii] = (REG && ok) ? o2_p[N + q] : T(0);
       }
 
-    // ---- vertical transposed FIR for computed rows [yc0, yc0+G) -> res (= P) ----
+    // ---- vertical transposed FIR for computed rows [yc0, yc0+G) -> res (= P):
+    //      lanes <-> column pairs (FFMA2), one (component, row block) per warp ----
     T* res = P;  // [2][G][RP], holds mbar = -K^T vbar
     constexpr int NBV = G / kRB;
-    constexpr int ICH = OX / 32;
-    for (int cb = warp; cb < 2 * NBV * ICH; cb += NW) {
-      const int ich = cb % ICH, jb = (cb / ICH) % NBV, c = cb / (ICH * NBV);
-      {
-        const int i = ich * 32 + lane;
-        const T* src = ring + c * RING * RP + (yc0 + jb * kRB - R - ring_lo) * RP + i;
-        T acc[kRB];
+    static_assert(2 * NBV == NW && OX == 64, "one (component, row block) per warp");
+    {
+      const int jb = warp % NBV, c = warp / NBV;
+      const int i = 2 * lane;
+      const float2* src = reinterpret_cast<const float2*>(
+          ring + c * RING * RP + (yc0 + jb * kRB - R - ring_lo) * RP + i);
+      float2 acc[kRB];
 #pragma unroll
-        for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < kRB + 2 * R; ++t) {
-          const T x = src[t * RP];
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const float2 x = src[t * (RP / 2)];
 #pragma unroll
-          for (int o = 0; o < kRB; ++o) {
-            const int tap = t - o;
-            if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
-          }
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
         }
-        const int gy0 = yc0 + jb * kRB;
-        if (gy0 <= 0 && gy0 + kRB > 0) {
-          const int o = -gy0;
-          T s = T(0);
-#pragma unroll
-          for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[(o + R + d) * RP], s);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-        }
-        if (gy0 <= H - 1 && gy0 + kRB > H - 1) {
-          const int o = H - 1 - gy0;
-          T s = T(0);
-#pragma unroll
-          for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[(o + R + d) * RP], s);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-        }
-#pragma unroll
-        for (int o = 0; o < kRB; ++o) res[c * G * RP + (jb * kRB + o) * RP + i] = -acc[o];
       }
+      const int gy0 = yc0 + jb * kRB;
+      if (gy0 <= 0 && gy0 + kRB > 0) {
+        const int o = -gy0;
+        float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int d = 0; d <= R; ++d) s2 = ffma2(src[(o + R + d) * (RP / 2)], (float)tp.e[R - d], s2);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+      }
+      if (gy0 <= H - 1 && gy0 + kRB > H - 1) {
+        const int o = H - 1 - gy0;
+        float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int d = -R; d <= 0; ++d) s2 = ffma2(src[(o + R + d) * (RP / 2)], (float)tp.e[R + d], s2);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+      }
+      float2* dst = reinterpret_cast<float2*>(res + c * G * RP + jb * kRB * RP + i);
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) dst[o * (RP / 2)] = make_float2(-acc[o].x, -acc[o].y);
     }
     mbar_wait(bar + 1, ph1);
     ph1 ^= 1u;
@@ -517,6 +555,39 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
     // ---- epilogue on owners: rows j in [1, G-1), cols i in [1, OX-1) ----
     const T* tI = epi0 + offE;
     const T* tz = tI + EPL;
+    T* __restrict__ zb_o = a.zb + b * N;
+    T* __restrict__ ib_o = a.ib + b * N;
+    // every owner >= 2 away from the image edges: central stencils, no edge terms
+    const bool interior = !REG && yc0 + 1 >= 2 && yc0 + G - 2 <= H - 3 && x_org + 1 >= 2 &&
+                          x_org + OX - 2 <= W - 3;
+    if (interior) {
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < NI; ++ii) {
+          const int j = 1 + warp + jj * NW, i = 1 + lane + ii * 32;
+          if (j >= G - 1 || i >= OX - 1) continue;
+          const int q = (yc0 + j) * W + (x_org + i);
+          const int e = j * OXP + i;
+          const T g0 = (tI[e + OXP] - tI[e - OXP]) / T(2);
+          const T g1 = (tI[e + 1] - tI[e - 1]) / T(2);
+          const T m0 = res[j * RP + i];
+          const T m1 = res[G * RP + j * RP + i];
+          zb_o[q] = pre_a[jj][ii] + (m0 * g0 + m1 * g1);  // objective.py:159
+          if (a.zero_a) {
+            a.zero_a[b * N + q] = T(0);
+            a.zero_b[b * N + q] = T(0);
+          }
+          // G^T(mbar z): 0.5 q[j-1] - 0.5 q[j+1] per axis (fields.py:148-158)
+          const T gm = res[(j - 1) * RP + i] * tz[e - OXP];
+          const T gp = res[(j + 1) * RP + i] * tz[e + OXP];
+          const T hm = res[G * RP + j * RP + i - 1] * tz[e - 1];
+          const T hp = res[G * RP + j * RP + i + 1] * tz[e + 1];
+          const T t0 = T(0.5) * gm - T(0.5) * gp;
+          const T t1 = T(0.5) * hm - T(0.5) * hp;
+          ib_o[q] = pre_b[jj][ii] + (t0 + t1);
+        }
+    } else {
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
@@ -525,7 +596,7 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
       const int gy = yc0 + j, gx = x_org + i;
       if (j >= G - 1 || i >= OX - 1 || gy >= H || gx >= W) continue;
       {
-        const long long q = (long long)gy * W + gx;
+        const int q = gy * W + gx;
         const int e = j * OXP + i;
         const T cI = tI[e];
         const T g0 = grad1(tI[e - OXP], cI, tI[e + OXP], gy, H);
@@ -539,7 +610,11 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
           a.zout[b * N + q] = zb_new;
           bad |= isfinite(zb_new) ? 0u : 1u;
         } else {
-          a.zb[b * N + q] = zb_new;
+          zb_o[q] = zb_new;
+          if (a.zero_a) {  // the consumed ibar/zbar of step k+1 = next step's scatter targets
+            a.zero_a[b * N + q] = T(0);
+            a.zero_b[b * N + q] = T(0);
+          }
           auto q0 = [&](int jr) { return res[jr * RP + i] * tz[jr * OXP + i]; };
           auto q1 = [&](int ic) { return res[G * RP + j * RP + ic] * tz[j * OXP + ic]; };
           const T zc = tz[e];
@@ -554,23 +629,25 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
           const T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
           const T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
           const T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
-          a.ib[b * N + q] = pre_b[jj][ii] + (t0 + t1);
+          ib_o[q] = pre_b[jj][ii] + (t0 + t1);
         }
       }
     }
+    }
     __syncthreads();
-    // ---- shift the ring by ADV rows ----
+    // ---- shift the ring by ADV rows (float4 copies, bands that never overlap) ----
     const int keep_lo = yc0 + ADV - R;  // first row needed by the next block
     constexpr int drop = ADV;           // == keep_lo - ring_lo
     constexpr int keep = G + 2 * R - ADV;  // == next_u - keep_lo
 #pragma unroll
     for (int band = 0; band < keep; band += drop) {
       const int nrow = (keep - band) < drop ? (keep - band) : drop;
-      for (int rr = band + warp; rr < band + nrow; rr += NW)
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          for (int i = lane; i < OX; i += 32)
-            ring[c * RING * RP + rr * RP + i] = ring[c * RING * RP + (rr + drop) * RP + i];
+      for (int t = tid; t < nrow * 2 * (OX / 4); t += kAdjStreamThreads) {
+        const int q4 = t % (OX / 4), rest = t / (OX / 4);
+        const int c = rest & 1, rr = band + (rest >> 1);
+        float4* dst = reinterpret_cast<float4*>(ring + c * RING * RP + rr * RP) + q4;
+        *dst = *(reinterpret_cast<const float4*>(ring + c * RING * RP + (rr + drop) * RP) + q4);
+      }
       __syncthreads();
     }
     ring_lo = keep_lo;
