@@ -405,6 +405,7 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
   T* cur = w;            // ibar | zbar   (2*S1)
   T* acc = w + 2 * S1;   // ib   | zb     (2*S1)
   T* vbar = w + 4 * S1;  // 2*S1
+  T* vtmp = w + 6 * S1;  // 2*S1: axis-0 pass of the split velocity adjoint
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)g.B, s) != cudaSuccess)
     return check_cuda("memset flags");
   rc = launch_cost_terms2d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
@@ -421,6 +422,7 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
     a.I = I + step * S1;
     a.z = z + step * S1;
     a.vbar = vbar;
+    a.vtmp = vtmp;
     a.ib = acc;
     a.zb = acc + S1;
     a.g = g;
@@ -610,7 +612,7 @@ size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g) {
   if (validate(dtype, g)) return 0;
   size_t es = dtype == MR_F32 ? 4 : 8;
   size_t S1 = (size_t)scalars(g);
-  return es * S1 * (g.ndim == 3 ? 11 : 6);
+  return es * S1 * (g.ndim == 3 ? 11 : 8);
 }
 
 int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps, double lam,

@@ -101,8 +101,48 @@ int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStre
   }
 }
 
+template <typename T, int R, bool TR, int EPI>
+int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
+                int32_t* guard, int guard_stride, cudaStream_t s);
+
+// Split velocity adjoint (fp32, scratch given): whole-column axis-0 transposed FIR
+// into a.vtmp (k_fir_axis0_f32), then the axis-1 pass + epilogue
+// (k_velocity_adj2d_h).  FIR work 2*(2R+1) FFMA per output plus the 1-px owner
+// overlap, against (2 + 2R/OX)*(2R+1) in the single-kernel tile engine.
+template <typename T, int R, bool REG>
+int veladj_split_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
+  if constexpr (sizeof(T) != 4) {
+    return 1;
+  } else {
+    if (!a.vtmp) return 1;
+    using S = FirSmem<T, R, 2>;
+    using V = VelAdjHSmem<R>;
+    VelAdjMaps m;
+    const long long B2 = 2LL * g.B;
+    const bool ok = make_map3<T>(&m.vbar, a.vtmp, g.W, g.H, B2, S::PX, S::OY) &&
+                    make_map3<T>(&m.I, a.I, g.W, g.H, g.B, V::OXP, S::OY) &&
+                    make_map3<T>(&m.z, a.z, g.W, g.H, g.B, V::OXP, S::OY);
+    if (!ok) return 1;
+    int rc = fir_axis0_r<T, R, true, 0>(tp, a.vbar, a.vtmp, (int)B2, g.H, (long long)g.W, nullptr,
+                                        0, s);
+    if (rc) return rc;
+    constexpr size_t bytes = V::bytes;
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_velocity_adj2d_h<R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (attr != cudaSuccess) return cuda_status(attr);
+    a.vbar = a.vtmp;
+    k_velocity_adj2d_h<R, REG>
+        <<<fir_grid(g.W, g.H, g.B, S::OX - 2, S::OY - 2), kThreads, bytes, s>>>(a, tp, m);
+    return cuda_status(cudaGetLastError());
+  }
+}
+
 template <typename T, int R, bool REG>
 int veladj_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
+  {
+    int rc = veladj_split_r<T, R, REG>(g, tp, a, s);
+    if (rc != 1) return rc;
+  }
   {
     int rc = veladj_stream_r<T, R, REG>(g, tp, a, s);
     if (rc != 1) return rc;
@@ -169,6 +209,16 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
 template <typename T, int R, bool TR, int EPI>
 int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
                 int32_t* guard, int guard_stride, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {  // fp32: FFMA2 engine, 64 x 64 tiles
+    constexpr size_t bytes = Ax0F32Smem<R>::bytes;
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_fir_axis0_f32<R, TR, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (attr != cudaSuccess) return cuda_status(attr);
+    dim3 grid((unsigned)((HW + kA0X - 1) / kA0X), (unsigned)((D + kA0D - 1) / kA0D), (unsigned)V);
+    k_fir_axis0_f32<R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
+                                                               tp);
+    return cuda_status(cudaGetLastError());
+  } else {
   constexpr size_t bytes = Ax0Smem<T, R>::bytes;
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_fir_axis0<T, R, TR, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -178,6 +228,7 @@ int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long 
   k_fir_axis0<T, R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
                                                             tp);
   return cuda_status(cudaGetLastError());
+  }
 }
 
 template <typename T>

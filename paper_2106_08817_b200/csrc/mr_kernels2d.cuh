@@ -50,6 +50,112 @@ struct FirSmem {
   static_assert(C * OY * OP <= region, "result must fit in the region buffer");
 };
 
+// Pass 2 of the FIR engine: along axis 1 over the pass-1 output vt [C][OY][VP]
+// (odd pitch, lanes <-> rows) into res [C][OY][OP]; transpose edge columns at
+// image columns 0 and n-1.
+template <typename T, int R, int C, bool TRANSPOSE>
+__device__ __forceinline__ void fir2d_pass2(const T* vt, T* res, const Taps<T>& tp, int x_org,
+                                            int W) {
+  using S = FirSmem<T, R, C>;
+  constexpr int OX = S::OX, OY = S::OY, VP = S::VP, OP = S::OP;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NB2 = OX / kRB;
+  static_assert(OY == 32, "pass 2 maps lanes to the 32 rows of a tile");
+  if constexpr (sizeof(T) == 4) {
+    // fp32: rows (j, j+16) packed per thread (FFMA2); half-warps take two column blocks
+    static_assert(NB2 % 2 == 0, "column blocks come in pairs");
+    for (int cb = warp; cb < C * NB2 / 2; cb += kNW) {
+      const int j = lane & 15;
+      const int ib = 2 * (cb % (NB2 / 2)) + (lane >> 4);
+      const int c = cb / (NB2 / 2);
+      const T* s0 = vt + (c * OY + j) * VP + ib * kRB;
+      const T* s1 = s0 + 16 * VP;
+      float2 acc[kRB];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kRB + 2 * R; ++t) {
+        const float2 x = make_float2(s0[t], s1[t]);
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+          const int tap = t - o;
+          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
+        }
+      }
+      if (TRANSPOSE) {
+        const int gx0 = x_org + ib * kRB;
+        if (gx0 <= 0 && gx0 + kRB > 0) {
+          const int o = -gx0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = 0; d <= R; ++d)
+            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R - d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+        if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
+          const int o = W - 1 - gx0;
+          float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = -R; d <= 0; ++d)
+            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R + d], s2);
+#pragma unroll
+          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
+        }
+      }
+      T* d0 = res + (c * OY + j) * OP + ib * kRB;
+      T* d1 = d0 + 16 * OP;
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        d0[o] = acc[o].x;
+        d1[o] = acc[o].y;
+      }
+    }
+  } else {
+  for (int cb = warp; cb < C * NB2; cb += kNW) {
+    const int j = lane;
+    const int ib = cb % NB2;
+    const int c = cb / NB2;
+    const T* src = vt + (c * OY + j) * VP + ib * kRB;
+    T acc[kRB];
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) acc[o] = T(0);
+#pragma unroll
+    for (int t = 0; t < kRB + 2 * R; ++t) {
+      T x = src[t];
+#pragma unroll
+      for (int o = 0; o < kRB; ++o) {
+        const int tap = t - o;
+        if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
+      }
+    }
+    if (TRANSPOSE) {
+      const int gx0 = x_org + ib * kRB;
+      if (gx0 <= 0 && gx0 + kRB > 0) {
+        const int o = -gx0;
+        T s = T(0);
+#pragma unroll
+        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[o + R + d], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+      if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
+        const int o = W - 1 - gx0;
+        T s = T(0);
+#pragma unroll
+        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[o + R + d], s);
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
+      }
+    }
+    T* dst = res + (c * OY + j) * OP + ib * kRB;
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
+  }
+  }
+}
+
 // Separable FIR passes over one staged tile.  rg holds the region
 // [c][RY][PX] covering output rows [y_org, y_org+OY) x cols [x_org, x_org+OX)
 // plus an R halo:
@@ -179,102 +285,8 @@ __device__ __forceinline__ const T* fir2d_passes(T* rg, T* vt, const Taps<T>& tp
   __syncthreads();
   mid();
 
-  // ---- pass 2: along axis 1 (columns); lanes <-> rows (odd pitch) ----
-  constexpr int NB2 = OX / kRB;
   T* res = rg;
-  static_assert(OY == 32, "pass 2 maps lanes to the 32 rows of a tile");
-  if constexpr (sizeof(T) == 4) {
-    // fp32: rows (j, j+16) packed per thread (FFMA2); half-warps take two column blocks
-    static_assert(NB2 % 2 == 0, "column blocks come in pairs");
-    for (int cb = warp; cb < C * NB2 / 2; cb += kNW) {
-      const int j = lane & 15;
-      const int ib = 2 * (cb % (NB2 / 2)) + (lane >> 4);
-      const int c = cb / (NB2 / 2);
-      const T* s0 = vt + (c * OY + j) * VP + ib * kRB;
-      const T* s1 = s0 + 16 * VP;
-      float2 acc[kRB];
-#pragma unroll
-      for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int t = 0; t < kRB + 2 * R; ++t) {
-        const float2 x = make_float2(s0[t], s1[t]);
-#pragma unroll
-        for (int o = 0; o < kRB; ++o) {
-          const int tap = t - o;
-          if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(x, (float)tp.w[tap], acc[o]);
-        }
-      }
-      if (TRANSPOSE) {
-        const int gx0 = x_org + ib * kRB;
-        if (gx0 <= 0 && gx0 + kRB > 0) {
-          const int o = -gx0;
-          float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int d = 0; d <= R; ++d)
-            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R - d], s2);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
-        }
-        if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
-          const int o = W - 1 - gx0;
-          float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int d = -R; d <= 0; ++d)
-            s2 = ffma2(make_float2(s0[o + R + d], s1[o + R + d]), (float)tp.e[R + d], s2);
-#pragma unroll
-          for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s2;
-        }
-      }
-      T* d0 = res + (c * OY + j) * OP + ib * kRB;
-      T* d1 = d0 + 16 * OP;
-#pragma unroll
-      for (int o = 0; o < kRB; ++o) {
-        d0[o] = acc[o].x;
-        d1[o] = acc[o].y;
-      }
-    }
-  } else {
-  for (int cb = warp; cb < C * NB2; cb += kNW) {
-    const int j = lane;
-    const int ib = cb % NB2;
-    const int c = cb / NB2;
-    const T* src = vt + (c * OY + j) * VP + ib * kRB;
-    T acc[kRB];
-#pragma unroll
-    for (int o = 0; o < kRB; ++o) acc[o] = T(0);
-#pragma unroll
-    for (int t = 0; t < kRB + 2 * R; ++t) {
-      T x = src[t];
-#pragma unroll
-      for (int o = 0; o < kRB; ++o) {
-        const int tap = t - o;
-        if (tap >= 0 && tap <= 2 * R) acc[o] = fma(tp.w[tap], x, acc[o]);
-      }
-    }
-    if (TRANSPOSE) {
-      const int gx0 = x_org + ib * kRB;
-      if (gx0 <= 0 && gx0 + kRB > 0) {
-        const int o = -gx0;
-        T s = T(0);
-#pragma unroll
-        for (int d = 0; d <= R; ++d) s = fma(tp.e[R - d], src[o + R + d], s);
-#pragma unroll
-        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-      }
-      if (gx0 <= W - 1 && gx0 + kRB > W - 1) {
-        const int o = W - 1 - gx0;
-        T s = T(0);
-#pragma unroll
-        for (int d = -R; d <= 0; ++d) s = fma(tp.e[R + d], src[o + R + d], s);
-#pragma unroll
-        for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = s;
-      }
-    }
-    T* dst = res + (c * OY + j) * OP + ib * kRB;
-#pragma unroll
-    for (int o = 0; o < kRB; ++o) dst[o] = acc[o];
-  }
-  }
+  fir2d_pass2<T, R, C, TRANSPOSE>(vt, res, tp, x_org, W);
   return res;
 }
 
@@ -858,6 +870,8 @@ struct VelAdjArgs {
   int use_tma;
   T* zero_a;       // nullable: buffers zeroed at the owner pixels (the consumed
   T* zero_b;       //   ibar/zbar of step k+1 = next step's scatter targets)
+  T* vtmp;         // nullable scratch [B][2][N]: enables the split path (axis-0 pass
+                   //   to vtmp, then the axis-1 pass + epilogue), fp32 only
   Grid2 g;
 };
 
@@ -1061,6 +1075,187 @@ __global__ void __launch_bounds__(kThreads)
   if (REG) {
     unsigned all = __reduce_or_sync(0xffffffffu, bad);
     if (all && (threadIdx.x & 31) == 0) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K4 split path, second kernel (fp32): the axis-0 transposed FIR already ran over
+// whole columns (k_fir_axis0_f32, no halo FLOPs) into a.vbar; this kernel stages
+// OY rows x (OX + 2R) columns of it by TMA (zero fill = the transpose's zero
+// padding along axis 1), copies them to the odd-pitch pass-2 buffer, runs the
+// axis-1 transposed FIR (fir2d_pass2) and the same epilogue as k_velocity_adj2d.
+// The owner operands zb, ib | v0 come from global memory into registers while
+// the FIR runs; I and z tiles (neighbours needed) arrive by TMA.
+// ------------------------------------------------------------------------------
+template <int R>
+struct VelAdjHSmem {
+  using S = FirSmem<float, R, 2>;
+  static constexpr int CSH = round_up(S::OY * S::PX, 32);    // staged rows per component
+  static constexpr int stage = round_up(2 * CSH + S::A, 32);
+  static constexpr int OXP = S::OX + S::A;                   // epilogue box width
+  static constexpr int OXY = round_up(OXP * S::OY, 32);
+  static constexpr int res = round_up(2 * S::OY * S::OP, 32);  // res at the start of rg
+  static constexpr int rg = stage > res + 2 * OXY + S::A ? stage : res + 2 * OXY + S::A;
+  static constexpr size_t head = 128;
+  static constexpr size_t bytes = head + sizeof(float) * (size_t)(rg + S::vt);
+};
+
+template <int R, bool REG>
+__global__ void __launch_bounds__(kThreads)
+    k_velocity_adj2d_h(VelAdjArgs<float> a, Taps<float> tp, const __grid_constant__ VelAdjMaps maps) {
+  using T = float;
+  using S = FirSmem<T, R, 2>;
+  using V = VelAdjHSmem<R>;
+  constexpr int OX = S::OX, OY = S::OY, OP = S::OP, RX = S::RX, PX = S::PX, VP = S::VP,
+                OXP = V::OXP, OXY = V::OXY, CSH = V::CSH;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  T* rg0 = reinterpret_cast<T*>(smem_raw + V::head);
+  T* vt = rg0 + V::rg;
+  T* res = rg0;                 // [2][OY][OP] after the copy
+  T* tail0 = rg0 + V::res;      // [2][OY][OXP]: I, z
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * (OX - 2) - 1, y_org = blockIdx.y * (OY - 2) - 1;
+  const int offV = align_shift(x_org - R, S::A), offE = align_shift(x_org, S::A);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_barrier_init();
+    mbar_expect_tx(bar, (unsigned)(sizeof(T) * 2 * PX * OY));
+    tma_load_3d(rg0, &maps.vbar, x_org - R - offV, y_org, 2 * b, bar);
+    tma_load_3d(rg0 + CSH, &maps.vbar, x_org - R - offV, y_org, 2 * b + 1, bar);
+  }
+  // owner operands into registers while the tile arrives and the FIR runs
+  constexpr int NJ = (OY - 2 + kNW - 1) / kNW, NI = (OX - 2 + 31) / 32;
+  T pre_a[NJ][NI], pre_b[NJ][NI], pre_c[NJ][NI];
+  const T* __restrict__ zb_p = a.zb + b * N;
+  const T* __restrict__ o2_p = REG ? a.v0 + b * 2 * N : a.ib + b * N;
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+    for (int ii = 0; ii < NI; ++ii) {
+      const int j = 1 + warp + jj * kNW, i = 1 + lane + ii * 32;
+      const int gy = y_org + j, gx = x_org + i;
+      const bool ok = j < OY - 1 && i < OX - 1 && gy < H && gx < W;
+      const int q = ok ? gy * W + gx : 0;  // < N < 2^31 per pair
+      pre_a[jj][ii] = ok ? zb_p[q] : T(0);
+      pre_b[jj][ii] = ok ? o2_p[q] : T(0);
+      pre_c[jj][ii] = (REG && ok) ? o2_p[N + q] : T(0);
+    }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // staged rows -> odd-pitch pass-2 input vt [2][OY][VP] (16-B loads, shifted scalar stores)
+  for (int rc = warp; rc < 2 * OY; rc += kNW) {
+    const int r = rc >> 1, c = rc & 1;
+    const float4* srow = reinterpret_cast<const float4*>(rg0 + c * CSH + r * PX);
+    T* vrow = vt + (c * OY + r) * VP - offV;  // staged element i -> vrow[i]
+    for (int q4 = lane; q4 < PX / 4; q4 += 32) {
+      const float4 v4 = srow[q4];
+      const int i = 4 * q4;
+      if (i >= offV && i < offV + RX) vrow[i] = v4.x;
+      if (i + 1 >= offV && i + 1 < offV + RX) vrow[i + 1] = v4.y;
+      if (i + 2 >= offV && i + 2 < offV + RX) vrow[i + 2] = v4.z;
+      if (i + 3 >= offV && i + 3 < offV + RX) vrow[i + 3] = v4.w;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // I and z tiles of the epilogue into the freed staging area
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(bar + 1, (unsigned)(sizeof(T) * OXP * OY * 2));
+    const int xa = x_org - offE;
+    tma_load_3d(tail0, &maps.I, xa, y_org, b, bar + 1);
+    tma_load_3d(tail0 + OXY, &maps.z, xa, y_org, b, bar + 1);
+  }
+  fir2d_pass2<T, R, 2, true>(vt, res, tp, x_org, W);
+  mbar_wait(bar + 1, 0);
+  __syncthreads();
+
+  const T* tI = tail0 + offE;
+  const T* tz = tI + OXY;
+  T* __restrict__ zb_o = a.zb + b * N;
+  T* __restrict__ ib_o = a.ib + b * N;
+  unsigned bad = 0;
+  const bool interior = !REG && y_org + 1 >= 2 && y_org + OY - 2 <= H - 3 && x_org + 1 >= 2 &&
+                        x_org + OX - 2 <= W - 3;
+  if (interior) {
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < NI; ++ii) {
+        const int j = 1 + warp + jj * kNW, i = 1 + lane + ii * 32;
+        if (j >= OY - 1 || i >= OX - 1) continue;
+        const int q = (y_org + j) * W + (x_org + i);
+        const int e = j * OXP + i;
+        const T g0 = (tI[e + OXP] - tI[e - OXP]) / T(2);
+        const T g1 = (tI[e + 1] - tI[e - 1]) / T(2);
+        const T m0 = -res[j * OP + i];
+        const T m1 = -res[(OY + j) * OP + i];
+        zb_o[q] = pre_a[jj][ii] + (m0 * g0 + m1 * g1);  // objective.py:159
+        if (a.zero_a) {
+          a.zero_a[b * N + q] = T(0);
+          a.zero_b[b * N + q] = T(0);
+        }
+        // G^T(mbar z): 0.5 q[j-1] - 0.5 q[j+1] per axis (fields.py:148-158)
+        const T gm = -res[(j - 1) * OP + i] * tz[e - OXP];
+        const T gp = -res[(j + 1) * OP + i] * tz[e + OXP];
+        const T hm = -res[(OY + j) * OP + i - 1] * tz[e - 1];
+        const T hp = -res[(OY + j) * OP + i + 1] * tz[e + 1];
+        const T t0 = T(0.5) * gm - T(0.5) * gp;
+        const T t1 = T(0.5) * hm - T(0.5) * hp;
+        ib_o[q] = pre_b[jj][ii] + (t0 + t1);
+      }
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < NI; ++ii) {
+        const int j = 1 + warp + jj * kNW, i = 1 + lane + ii * 32;
+        const int gy = y_org + j, gx = x_org + i;
+        if (j >= OY - 1 || i >= OX - 1 || gy >= H || gx >= W) continue;
+        const int q = gy * W + gx;
+        const int e = j * OXP + i;
+        const T c = tI[e];
+        const T g0 = grad1(tI[e - OXP], c, tI[e + OXP], gy, H);
+        const T g1 = grad1(tI[e - 1], c, tI[e + 1], gx, W);
+        const T m0 = -res[j * OP + i];
+        const T m1 = -res[(OY + j) * OP + i];
+        T zb_new = pre_a[jj][ii] + (m0 * g0 + m1 * g1);  // objective.py:159
+        if (REG) {
+          // + lam*(K m0 . grad I0 + 2 rho z0) with K m0 = -v0 (objective.py:165-169)
+          const T km = -(pre_b[jj][ii] * g0 + pre_c[jj][ii] * g1);
+          zb_new = zb_new + a.lam * (km + a.two_rho * tz[e]);
+          a.zout[b * N + q] = zb_new;
+          bad |= isfinite(zb_new) ? 0u : 1u;
+        } else {
+          zb_o[q] = zb_new;
+          if (a.zero_a) {
+            a.zero_a[b * N + q] = T(0);
+            a.zero_b[b * N + q] = T(0);
+          }
+          auto q0 = [&](int jr) { return -res[jr * OP + i] * tz[jr * OXP + i]; };
+          auto q1 = [&](int ic) { return -res[(OY + j) * OP + ic] * tz[j * OXP + ic]; };
+          const T zc = tz[e];
+          const T qc0 = m0 * zc, qc1 = m1 * zc;
+          const T gm = (gy > 0) ? q0(j - 1) : T(0);
+          const T gp = (gy < H - 1) ? q0(j + 1) : T(0);
+          const T gf = (gy == 0) ? qc0 : ((gy == 1) ? gm : T(0));
+          const T gl = (gy == H - 1) ? qc0 : ((gy == H - 2) ? gp : T(0));
+          const T t0 = diff_adj1(gm, gp, gf, gl, gy, H);
+          const T hm = (gx > 0) ? q1(i - 1) : T(0);
+          const T hp = (gx < W - 1) ? q1(i + 1) : T(0);
+          const T hf = (gx == 0) ? qc1 : ((gx == 1) ? hm : T(0));
+          const T hl = (gx == W - 1) ? qc1 : ((gx == W - 2) ? hp : T(0));
+          const T t1 = diff_adj1(hm, hp, hf, hl, gx, W);
+          ib_o[q] = pre_b[jj][ii] + (t0 + t1);
+        }
+      }
+  }
+  if (REG) {
+    unsigned all = __reduce_or_sync(0xffffffffu, bad);
+    if (all && lane == 0) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
   }
 }
 
