@@ -67,7 +67,11 @@ __device__ __forceinline__ void fir2d_pass2(const T* vt, T* res, const Taps<T>& 
     static_assert(NB2 % 2 == 0, "column blocks come in pairs");
     for (int cb = warp; cb < C * NB2 / 2; cb += kNW) {
       const int j = lane & 15;
-      const int ib = 2 * (cb % (NB2 / 2)) + (lane >> 4);
+      // half-warps take column blocks 16 columns apart: with the odd pitch the two
+      // halves' 16 rows then fall in complementary bank sets (conflict-free)
+      static_assert(NB2 == 8, "column-block pairing assumes 8 blocks");
+      const int pb = cb % (NB2 / 2);
+      const int ib = (pb & 1) + 4 * (pb >> 1) + 2 * (lane >> 4);
       const int c = cb / (NB2 / 2);
       const T* s0 = vt + (c * OY + j) * VP + ib * kRB;
       const T* s1 = s0 + 16 * VP;
@@ -1147,19 +1151,14 @@ __global__ void __launch_bounds__(kThreads)
     }
   __syncthreads();
   mbar_wait(bar, 0);
-  // staged rows -> odd-pitch pass-2 input vt [2][OY][VP] (16-B loads, shifted scalar stores)
+  // staged rows -> odd-pitch pass-2 input vt [2][OY][VP] (consecutive lanes on both
+  // sides: conflict-free loads and stores)
   for (int rc = warp; rc < 2 * OY; rc += kNW) {
     const int r = rc >> 1, c = rc & 1;
-    const float4* srow = reinterpret_cast<const float4*>(rg0 + c * CSH + r * PX);
-    T* vrow = vt + (c * OY + r) * VP - offV;  // staged element i -> vrow[i]
-    for (int q4 = lane; q4 < PX / 4; q4 += 32) {
-      const float4 v4 = srow[q4];
-      const int i = 4 * q4;
-      if (i >= offV && i < offV + RX) vrow[i] = v4.x;
-      if (i + 1 >= offV && i + 1 < offV + RX) vrow[i + 1] = v4.y;
-      if (i + 2 >= offV && i + 2 < offV + RX) vrow[i + 2] = v4.z;
-      if (i + 3 >= offV && i + 3 < offV + RX) vrow[i + 3] = v4.w;
-    }
+    const T* srow = rg0 + c * CSH + r * PX + offV;
+    T* vrow = vt + (c * OY + r) * VP;
+#pragma unroll
+    for (int i = lane; i < RX; i += 32) vrow[i] = srow[i];
   }
   __syncthreads();
   if (tid == 0) {  // I and z tiles of the epilogue into the freed staging area

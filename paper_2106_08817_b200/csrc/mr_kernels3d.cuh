@@ -219,26 +219,30 @@ __global__ void __launch_bounds__(kThreads)
   const float* __restrict__ src = in + (long long)vol * D * HW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
-  for (int t = threadIdx.x; t < RD * (kA0X / 4); t += kThreads) {
-    const int j = t / (kA0X / 4), q = t % (kA0X / 4);
-    int gd = d_org - R + j;
-    bool rin = true;
-    if (TRANSPOSE) {
-      rin = gd >= 0 && gd < D;
-      gd = rin ? gd : 0;
-    } else {
-      gd = min(max(gd, 0), D - 1);
-    }
-    const float* row = src + (long long)gd * HW;
-    const long long gx = x0 + 4 * q;
-    float* dst = rgf + j * kA0X + 4 * q;
-    if (vec && gx + 3 < HW) {
-      cp_async16_zfill(dst, row + gx, rin);
-    } else {
+  {
+    // 16 lanes per row (one 16-B chunk each), 16 rows per pass of the CTA
+    const int c4 = threadIdx.x & 15;
+    const long long gx = x0 + 4 * c4;
+    const bool full = vec && gx + 3 < HW;
+    float* dst = rgf + 4 * c4;
+    for (int j = threadIdx.x >> 4; j < RD; j += kThreads / 16) {
+      int gd = d_org - R + j;
+      bool rin = true;
+      if (TRANSPOSE) {
+        rin = gd >= 0 && gd < D;
+        gd = rin ? gd : 0;
+      } else {
+        gd = min(max(gd, 0), D - 1);
+      }
+      const float* row = src + (long long)gd * HW + gx;
+      if (full) {
+        cp_async16_zfill(dst + j * kA0X, row, rin);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool ok = rin && gx + e < HW;
-        cp_async_elem_zfill(dst + e, row + (ok ? gx + e : 0), ok);
+        for (int e = 0; e < 4; ++e) {
+          const bool ok = rin && gx + e < HW;
+          cp_async_elem_zfill(dst + j * kA0X + e, ok ? row + e : src, ok);
+        }
       }
     }
   }
@@ -282,10 +286,10 @@ __global__ void __launch_bounds__(kThreads)
   const long long gx = x0 + i;
   unsigned flags = 0;
   if (gx < HW) {
-    float* dst = out + (long long)vol * D * HW + gx;
+    float* p = out + (long long)vol * D * HW + (long long)gd0 * HW + gx;
     const bool pair = gx + 1 < HW && ((HW & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
 #pragma unroll
-    for (int o = 0; o < kRB; ++o) {
+    for (int o = 0; o < kRB; ++o, p += HW) {
       const int gd = gd0 + o;
       if (gd < D) {
         float2 val = acc[o];
@@ -296,7 +300,6 @@ __global__ void __launch_bounds__(kThreads)
             if (gx + 1 < HW) flags |= guard_bits(val.y, MR_GUARD_VELOCITY_NONFINITE);
           }
         }
-        float* p = dst + (long long)gd * HW;
         if (pair) {
           *reinterpret_cast<float2*>(p) = val;
         } else {

@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(kThreads)
         constexpr int NB = OX / kRB;
         for (int cb = warp; cb < NB; cb += kNW) {  // (c, column-block pair)
           const int r = lane & 15;
-          const int ib = 2 * (cb % (NB / 2)) + (lane >> 4);
+          // half-warps 16 columns apart: complementary bank sets with the odd pitch
+          const int pb = cb % (NB / 2);
+          const int ib = (pb & 1) + 4 * (pb >> 1) + 2 * (lane >> 4);
           const int c = cb / (NB / 2);
           if (r >= cin) continue;
           const T* s0 = P + c * G * PP + r * PP + ib * kRB;
@@ -403,20 +405,13 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
       mbar_wait(bar, ph0);
       ph0 ^= 1u;
       // vbar rows -> odd-pitch P (zeros outside the image came from the TMA fill)
-      // (16-B loads of the aligned staged row, scalar stores to the shifted odd-pitch row)
-      static_assert(PXZ % 4 == 0, "staged rows are 16-B aligned");
+      // (consecutive lanes on both sides: conflict-free loads and stores)
       for (int rc = warp; rc < 2 * cin; rc += NW) {
         const int r = rc >> 1, c = rc & 1;
-        const float4* srow = reinterpret_cast<const float4*>(st0 + c * C::n_st1 + r * PXZ);
-        T* prow = P + c * G * PP + r * PP - offV;  // staged element i -> prow[i]
-        for (int q4 = lane; q4 < PXZ / 4; q4 += 32) {
-          const float4 v4 = srow[q4];
-          const int i = 4 * q4;
-          if (i >= offV && i < offV + RX) prow[i] = v4.x;
-          if (i + 1 >= offV && i + 1 < offV + RX) prow[i + 1] = v4.y;
-          if (i + 2 >= offV && i + 2 < offV + RX) prow[i + 2] = v4.z;
-          if (i + 3 >= offV && i + 3 < offV + RX) prow[i + 3] = v4.w;
-        }
+        const T* srow = st0 + c * C::n_st1 + r * PXZ + offV;
+        T* prow = P + c * G * PP + r * PP;
+#pragma unroll
+        for (int i = lane; i < RX; i += 32) prow[i] = srow[i];
       }
       __syncthreads();
       const int nu = u0 + cnt;
@@ -430,7 +425,8 @@ __global__ void __launch_bounds__(kAdjStreamThreads)
       {
         const int cb = warp;
         const int r = lane & 15;
-        const int ib = 2 * (cb % (NB / 2)) + (lane >> 4);
+        const int pb = cb % (NB / 2);
+        const int ib = (pb & 1) + 4 * (pb >> 1) + 2 * (lane >> 4);
         const int c = cb / (NB / 2);
         if (r < cin) {
           const T* s0 = P + c * G * PP + r * PP + ib * kRB;
