@@ -60,6 +60,17 @@ int velocity_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) 
 template <typename T, int R, bool TR>
 int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStream_t s) {
   using S = FirSmem<T, R, 1>;
+  if constexpr (sizeof(T) == 4) {  // TMA-staged region when the layout is describable
+    CUtensorMap m;
+    if (g.N < (1LL << 31) && make_map3<T>(&m, a.a, g.W, g.H, g.B, S::PX, S::RY)) {
+      constexpr size_t bytes = SmoothTmaSmem<R>::bytes;
+      static const cudaError_t attr = cudaFuncSetAttribute(
+          k_smooth2d_tma<R, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (attr != cudaSuccess) return cuda_status(attr);
+      k_smooth2d_tma<R, TR><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, bytes, s>>>(a, tp, m);
+      return cuda_status(cudaGetLastError());
+    }
+  }
   static const cudaError_t attr = cudaFuncSetAttribute(
       k_smooth2d<T, R, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
   if (attr != cudaSuccess) return cuda_status(attr);

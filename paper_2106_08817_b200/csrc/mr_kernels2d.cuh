@@ -533,6 +533,71 @@ __global__ void __launch_bounds__(kThreads) k_smooth2d(SmoothArgs<T> a, Taps<T> 
   }
 }
 
+// TMA-staged variant (fp32): the whole region (tile + R halo) arrives as one box;
+// the box's zero fill outside the image is the transpose's zero padding, and for
+// the forward FIR border tiles copy each out-of-image element from its clamped
+// (in-image, in-region) source = replicate borders.  Then the same FIR passes.
+template <int R>
+struct SmoothTmaSmem {
+  using S = FirSmem<float, R, 1>;
+  static constexpr size_t head = 128;
+  static constexpr size_t bytes = head + S::bytes;
+};
+
+template <int R, bool TRANSPOSE>
+__global__ void __launch_bounds__(kThreads)
+    k_smooth2d_tma(SmoothArgs<float> a, Taps<float> tp, const __grid_constant__ CUtensorMap map) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using S = FirSmem<float, R, 1>;
+  constexpr int RX = S::RX, RY = S::RY, PX = S::PX;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  float* rg0 = reinterpret_cast<float*>(smem_raw + SmoothTmaSmem<R>::head);
+  float* vt = rg0 + S::region;
+  const int H = a.g.H, W = a.g.W;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * S::OX, y_org = blockIdx.y * S::OY;
+  const int xs = x_org - R, ys = y_org - R;
+  const int offV = align_shift(xs, S::A);
+  float* rg = rg0 + offV;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(bar, (unsigned)(sizeof(float) * PX * RY));
+    tma_load_3d(rg0, &map, xs - offV, ys, b, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  if (!TRANSPOSE && (xs < 0 || ys < 0 || xs + RX > W || ys + RY > H)) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int jlo = max(0, -ys), jhi = min(RY, H - ys);  // in-image rows [jlo, jhi)
+    const int ilo = max(0, -xs), ihi = min(RX, W - xs);  // in-image columns [ilo, ihi)
+    if (ilo > 0 || ihi < RX) {  // 1) out-of-image columns of in-image rows
+      const int nl = ilo, nr = RX - ihi;
+      for (int j = jlo + warp; j < jhi; j += kNW)
+        for (int t = lane; t < nl + nr; t += 32) {
+          const int i = t < nl ? t : ihi + (t - nl);
+          rg[j * PX + i] = rg[j * PX + (t < nl ? ilo : ihi - 1)];
+        }
+      __syncthreads();
+    }
+    // 2) out-of-image rows copy their clamped row (whole width, columns already fixed)
+    for (int j = warp; j < RY; j += kNW) {
+      if (j >= jlo && j < jhi) continue;
+      const int src = j < jlo ? jlo : jhi - 1;
+      for (int i = lane; i < RX; i += 32) rg[j * PX + i] = rg[src * PX + i];
+    }
+    __syncthreads();
+  }
+  const float* res = fir2d_passes<float, R, 1, TRANSPOSE>(rg, vt, tp, x_org, y_org, H, W, NoMid{});
+  __syncthreads();
+  float* dst = a.out + b * a.g.N;
+  for (int p = threadIdx.x; p < S::OX * S::OY; p += kThreads) {
+    const int j = p / S::OX, i = p - j * S::OX;
+    const int gy = y_org + j, gx = x_org + i;
+    if (gy < H && gx < W) dst[gy * W + gx] = res[j * S::OP + i];
+  }
+}
+
 // ------------------------------------------------------------------------------
 // K2: one semi-Lagrangian step (integrator.py:101-110, 193-205)
 // ------------------------------------------------------------------------------

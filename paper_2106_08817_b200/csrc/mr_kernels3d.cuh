@@ -532,6 +532,9 @@ __device__ __forceinline__ void scatter8_merged(T* __restrict__ out, int base, b
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
+  // Latency-bound gathers: every load (v and its neighbours, ibar/zbar, the 8+8
+  // corners of I and z, the s neighbours) is issued before the first scatter, so
+  // they are all in flight together instead of behind the atomics.
   const Grid3 g = a.g;
   const Vox vx_ = vox3(g);
   const bool own = vx_.ok;
@@ -544,17 +547,48 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   const T* __restrict__ v2 = v1 + g.N;
   const T* __restrict__ s = a.s + b * g.N;
   const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
+  const T ib_ = a.ibar[b * g.N + q], zb_ = a.zbar[b * g.N + q];
+  const T vm0 = d > 0 ? v0[q - g.HW] : a0, vp0 = d < g.D - 1 ? v0[q + g.HW] : a0;
+  const T vm1 = y > 0 ? v1[q - g.W] : a1, vp1 = y < g.H - 1 ? v1[q + g.W] : a1;
+  const T vm2 = x > 0 ? v2[q - 1] : a2, vp2 = x < g.W - 1 ? v2[q + 1] : a2;
+  const int st[3] = {(int)g.HW, g.W, 1};
+  const int pos[3] = {d, y, x};
+  const int n[3] = {g.D, g.H, g.W};
+  T sm[3], sp[3];
+  const T sc = s[q];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    sm[c] = pos[c] > 0 ? s[q - st[c]] : T(0);
+    sp[c] = pos[c] < n[c] - 1 ? s[q + st[c]] : T(0);
+  }
   const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
   const int base = (int)p.base;
-  const T ib_ = a.ibar[b * g.N + q], zb_ = a.zbar[b * g.N + q];
+  T cI[8], cz[8];
+  corners8(I, p, g, cI);
+  corners8(z, p, g, cz);
+
   T w8[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) w8[c] = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
-  const T div =
-      grad1(d > 0 ? v0[q - g.HW] : a0, a0, d < g.D - 1 ? v0[q + g.HW] : a0, d, g.D) +
-      grad1(y > 0 ? v1[q - g.W] : a1, a1, y < g.H - 1 ? v1[q + g.W] : a1, y, g.H) +
-      grad1(x > 0 ? v2[q - 1] : a2, a2, x < g.W - 1 ? v2[q + 1] : a2, x, g.W);
+  const T div = grad1(vm0, a0, vp0, d, g.D) + grad1(vm1, a1, vp1, y, g.H) +
+                grad1(vm2, a2, vp2, x, g.W);
   const T wz = zb_ * (T(1) - a.dt * div);
+  T dI[3], dz[3];
+  coord_grad3(cI, p, dI);
+  coord_grad3(cz, p, dz);
+  T vb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {  // vbar_c += D_c^T s (gather form along each axis)
+    const int j = pos[c];
+    const T sf = j == 0 ? sc : (j == 1 ? sm[c] : T(0));
+    const T sl = j == n[c] - 1 ? sc : (j == n[c] - 2 ? sp[c] : T(0));
+    vb[c] += diff_adj1(sm[c], sp[c], sf, sl, j, n[c]);
+  }
+
   T* __restrict__ ibo = a.ib + b * g.N;
   T* __restrict__ zbo = a.zb + b * g.N;
   T cw[8];
@@ -566,30 +600,6 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   scatter8_merged(zbo, base, own, g, cw);
   if (!own) return;
   if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
-  T cv[8], dI[3], dz[3];
-  corners8(I, p, g, cv);
-  coord_grad3(cv, p, dI);
-  corners8(z, p, g, cv);
-  coord_grad3(cv, p, dz);
-  T vb[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
-  {  // vbar_c += D_c^T s (gather form along each axis)
-    const int st[3] = {(int)g.HW, g.W, 1};
-    const int pos[3] = {d, y, x};
-    const int n[3] = {g.D, g.H, g.W};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int j = pos[c];
-      const T sm = j > 0 ? s[q - st[c]] : T(0);
-      const T sp = j < n[c] - 1 ? s[q + st[c]] : T(0);
-      const T sf = j == 0 ? s[q] : (j == 1 ? sm : T(0));
-      const T sl = j == n[c] - 1 ? s[q] : (j == n[c] - 2 ? sp : T(0));
-      vb[c] += diff_adj1(sm, sp, sf, sl, j, n[c]);
-    }
-  }
   if (a.reg_lam != T(0)) {
     T g0, g1, g2;
     grad3(I, q, d, y, x, g, g0, g1, g2);

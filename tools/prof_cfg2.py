@@ -16,6 +16,10 @@ p.add_argument("--batch", type=int, default=None)
 p.add_argument("--iters", type=int, default=2)
 a = p.parse_args()
 c = make_config(a.config, batch=a.batch)
+if a.config in (3, 4, 5):  # as bench.py: scale z0 until the shoot stays below the guard
+    from paper_2106_08817_b200.calibrate import calibrate_no_divergence
+
+    calibrate_no_divergence(c)
 bg = engine.BatchGrad(c.batch, c.shape, c.n_steps, c.mu, c.weights(), c.lam, c.rho)
 dt = torch.float32
 bg.load(torch.as_tensor(c.source, dtype=dt), torch.as_tensor(c.target, dtype=dt),
