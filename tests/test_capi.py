@@ -48,8 +48,8 @@ def test_library_rejects_bad_arguments_without_gpu():
     g = _lib.make_grid(1, (8, 8))
     k = _lib.MrKernel()
     k.radius = 40
-    assert lib.mr_adjoint_workspace_bytes(0, g) == 8 * 8 * 6 * 4
-    assert lib.mr_adjoint_workspace_bytes(1, g) == 8 * 8 * 6 * 8
+    assert lib.mr_adjoint_workspace_bytes(0, g) == 8 * 8 * 8 * 4
+    assert lib.mr_adjoint_workspace_bytes(1, g) == 8 * 8 * 8 * 8
     with pytest.raises(Exception):
         _lib.KernelHandle(np.ones(81) / 81)  # radius 40 > MR_MAX_RADIUS
 
