@@ -316,6 +316,7 @@ def kernel_times(bg, w, stream, reps: int = 1) -> dict:
     sI = torch.empty_like(traj.I[0])
     sz = torch.empty_like(traj.z[0])
     sv = torch.empty_like(traj.v[0])
+    ws = torch.empty_like(traj.v[0])  # 2 scalars per pixel: the split kernels the step runs
     out = {}
 
     def timed(name, fn, n):
@@ -329,7 +330,7 @@ def kernel_times(bg, w, stream, reps: int = 1) -> dict:
         out[name] = e0.elapsed_time(e1) / n
 
     timed("velocity", lambda k: _lib.check(lib.mr_velocity(
-        dt, g, kern.struct, P(traj.I[k]), P(traj.z[k]), P(sv), None, sp)), T + 1)
+        dt, g, kern.struct, P(traj.I[k]), P(traj.z[k]), P(sv), None, P(ws), sp)), T + 1)
     timed("sl_step", lambda k: _lib.check(lib.mr_sl_step(
         dt, g, 1.0 / T, bg.mu, P(traj.I[k]), P(traj.z[k]), P(traj.v[k]), P(sI), P(sz), None,
         None, sp)), T)
@@ -337,7 +338,7 @@ def kernel_times(bg, w, stream, reps: int = 1) -> dict:
         dt, g, 1.0 / T, bg.mu, P(traj.I[k]), P(traj.z[k]), P(traj.v[k]), P(traj.I[k + 1]),
         P(traj.z[k + 1]), P(sI), P(sz), P(sv), sp)), T)
     timed("velocity_adjoint", lambda k: _lib.check(lib.mr_velocity_adjoint(
-        dt, g, kern.struct, P(traj.I[k]), P(traj.z[k]), P(traj.v[k]), P(sI), P(sz), sp)), T)
+        dt, g, kern.struct, P(traj.I[k]), P(traj.z[k]), P(traj.v[k]), P(sI), P(sz), P(ws), sp)), T)
     return out
 
 

@@ -77,11 +77,14 @@ typedef struct {
 /* v = -K * (z grad I) for every pair.  Replaces velocity_from_momentum /
  * velocity_arr (integrator.py:93-94, 124-130), i.e. gradient_arr
  * (fields.py:161-162) + smooth_vec_arr (kernel.py:82-85).
+ * workspace: nullable device scratch of 2 scalars per pixel; when given, the
+ * fp32 path runs as two kernels (product + axis-1 pass, then the axis-0 pass
+ * over whole columns) instead of one; the result is the same operator.
  * guard: nullable int32[B]; OR-ed with the MR_GUARD_VELOCITY_* bits of v
  * (_guard, integrator.py:113-118; mr_shoot_forward guards I and z in the
  * transport step that produces them). */
 int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
-                void* v, int32_t* guard, void* stream);
+                void* v, int32_t* guard, void* workspace, void* stream);
 
 /* One semi-Lagrangian step (integrator.py:193-205):
  *   plan  = bilinear_plan(Id - dt v)            fields.py:207-224
@@ -103,15 +106,19 @@ int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu,
 /* Adjoint of v = -K*(z grad I) -- objective.py:157-161:
  *   mbar = -K^T vbar (smooth_adjoint_vec_arr, kernel.py:48-68, 88-92)
  *   zb  += sum_c mbar_c d_c I ;  ib += G^T(mbar z) (fields.py:148-166)
- * ib/zb are read-modify-write ([B][N]). */
+ * ib/zb are read-modify-write ([B][N]).  workspace: nullable, 2 scalars per
+ * pixel; when given, the fp32 path runs the axis-0 transposed FIR over whole
+ * columns first (split kernels), as mr_shoot_adjoint does. */
 int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I,
                         const void* z, const void* vbar, void* ib, void* zb,
-                        void* stream);
+                        void* workspace, void* stream);
 
 /* ---- whole-loop entry points (one call per shoot / gradient) -------------- */
 
-/* Bytes of device workspace mr_shoot_forward needs (0 in 2D; 3 scalars per
- * voxel in 3D, where the separable smoothing round-trips through it). */
+/* Bytes of device workspace mr_shoot_forward uses: 3 scalars per voxel in 3D,
+ * where the separable smoothing round-trips through it (required); 2 scalars
+ * per pixel in 2D, where it holds the axis-1 pass of the split fp32 velocity
+ * (optional: NULL keeps the single-kernel velocity). */
 size_t mr_forward_workspace_bytes(int dtype, mr_grid g);
 
 /* shoot() for Scheme.SEMI_LAGRANGIAN (integrator.py:163-219), every pair of

@@ -62,10 +62,10 @@ _i32 = ctypes.c_int32
 _d = ctypes.c_double
 
 _SIGNATURES = {
-    "mr_velocity": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp]),
+    "mr_velocity": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_sl_step": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_sl_step_adjoint": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "mr_velocity_adjoint": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_velocity_adjoint": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_shoot_forward": (_i32, [_i32, MrGrid, MrKernel, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_forward_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
     "mr_adjoint_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),

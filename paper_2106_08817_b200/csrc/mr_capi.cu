@@ -131,7 +131,7 @@ static int velocity3d(const Grid3& g, int R, const Taps<T>& tp, const T* I, cons
   Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};  // every (pair, component, slice) as a 2D image
   rc = launch_smooth2d<T>(sl, R, tp, v, tmp, false, s);
   if (rc) return rc;
-  return launch_fir_axis0<T>(R, tp, tmp, v, g.B * 3, g.D, g.HW, false, 1, guard, guard_stride, s);
+  return launch_fir_axis0<T>(R, tp, tmp, v, g.B * 3, g.D, g.HW, false, 1, guard, guard_stride, 3, s);
 }
 
 template <typename T>
@@ -278,9 +278,12 @@ static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T
   }
   if (guard && cudaMemsetAsync(guard, 0, sizeof(int32_t) * (size_t)g.B * (T_ + 1), s) != cudaSuccess)
     return check_cuda("memset guard");
+  // split velocity (two kernels, whole-column axis-0 pass) once its 64 x 32 tiles
+  // fill the GPU twice; the single-kernel path below that (launch-bound sizes)
+  if ((long long)((g.W + 63) / 64) * ((g.H + 31) / 32) * g.B < 2 * 148) ws = nullptr;
   for (int step = 0; step < T_; ++step) {
     rc = launch_velocity2d<T>(g, k.radius, tp, I + step * S1, z + step * S1, v + step * SV,
-                              guard ? guard + step : nullptr, T_ + 1, s);
+                              guard ? guard + step : nullptr, T_ + 1, s, static_cast<T*>(ws));
     if (rc) return check_rc(rc, "velocity");
     rc = launch_sl_step2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV,
                              I + (step + 1) * S1, z + (step + 1) * S1, ph[step & 1],
@@ -290,7 +293,7 @@ static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T
     if (rc) return check_rc(rc, "sl_step");
   }
   rc = launch_velocity2d<T>(g, k.radius, tp, I + T_ * S1, z + T_ * S1, v + T_ * SV,
-                            guard ? guard + T_ : nullptr, T_ + 1, s);
+                            guard ? guard + T_ : nullptr, T_ + 1, s, static_cast<T*>(ws));
   if (rc) return check_rc(rc, "velocity");
   return MR_OK;
 }
@@ -350,7 +353,7 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
     k_sl_adjoint3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
     if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "sl_adjoint3d");
     // ktv = K^T vbar: axis 0 first, then axes 1, 2 per slice (kernel.py:76-79 order)
-    rc = launch_fir_axis0<T>(k.radius, tp, vbar, tmp, g.B * 3, g.D, g.HW, true, 0, nullptr, 1, s);
+    rc = launch_fir_axis0<T>(k.radius, tp, vbar, tmp, g.B * 3, g.D, g.HW, true, 0, nullptr, 1, 3, s);
     if (rc) return check_rc(rc, "fir_axis0^T");
     rc = launch_smooth2d<T>(sl, k.radius, tp, tmp, vbar, true, s);
     if (rc) return check_rc(rc, "smooth2d^T");
@@ -470,7 +473,7 @@ const char* mr_strerror(int code) {
 #define MR_DISPATCH(dtype, CALL_F32, CALL_F64) ((dtype) == MR_F32 ? (CALL_F32) : (CALL_F64))
 
 int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z, void* v,
-                int32_t* guard, void* stream) {
+                int32_t* guard, void* workspace, void* stream) {
   int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!I || !z || !v) return fail(MR_EINVAL, "NULL field pointer");
@@ -479,7 +482,7 @@ int mr_velocity(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
     Taps<float> tp;
     if ((rc = make_taps<float>(k, tp))) return rc;
     rc = launch_velocity2d<float>(g2, k.radius, tp, (const float*)I, (const float*)z, (float*)v,
-                                  guard, 1, as_stream(stream));
+                                  guard, 1, as_stream(stream), (float*)workspace);
   } else {
     Taps<double> tp;
     if ((rc = make_taps<double>(k, tp))) return rc;
@@ -562,7 +565,7 @@ int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu, const void* I
 }
 
 int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const void* z,
-                        const void* vbar, void* ib, void* zb, void* stream) {
+                        const void* vbar, void* ib, void* zb, void* workspace, void* stream) {
   int rc = validate(dtype, g, false);
   if (rc) return rc;
   if (!I || !z || !vbar || !ib || !zb) return fail(MR_EINVAL, "NULL field pointer");
@@ -573,6 +576,7 @@ int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const 
     VelAdjArgs<float> a{};
     a.I = (const float*)I; a.z = (const float*)z; a.vbar = (const float*)vbar;
     a.ib = (float*)ib; a.zb = (float*)zb; a.g = g2;
+    a.vtmp = (float*)workspace;
     rc = launch_velocity_adj2d<float>(g2, k.radius, tp, a, false, as_stream(stream));
   } else {
     Taps<double> tp;
@@ -587,8 +591,9 @@ int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I, const 
 
 size_t mr_forward_workspace_bytes(int dtype, mr_grid g) {
   if (validate(dtype, g)) return 0;
-  if (g.ndim == 2) return 0;
-  return (size_t)(dtype == MR_F32 ? 4 : 8) * (size_t)scalars(g) * 3;
+  // 2D: optional (NULL keeps the single-kernel velocity); 2 scalars per pixel
+  // hold the axis-1 pass of the split fp32 velocity.  3D: 3 scalars per voxel.
+  return (size_t)(dtype == MR_F32 ? 4 : 8) * (size_t)scalars(g) * (g.ndim == 2 ? 2 : 3);
 }
 
 int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps,

@@ -37,8 +37,43 @@ int velocity_stream_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStrea
   }
 }
 
+template <typename T, int R, bool TR, int EPI>
+int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
+                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s);
+
+// Split velocity (fp32, scratch given): product +
+// axis-1 FIR per tile (k_velocity2d_h) into a.vtmp, then the axis-0 FIR over whole
+// columns with negate + velocity guard (k_fir_axis0_f32<R, false, 1>).
+template <typename T, int R>
+int velocity_split_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
+  if constexpr (sizeof(T) != 4) {
+    return 1;
+  } else {
+    using S = FirSmem<T, R, 2>;
+    using V = VelHSmem<R>;
+    if (!a.vtmp) return 1;
+    CUtensorMap mI, mZ;
+    if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, V::PXI, S::OY + 2) ||
+        !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, V::PXZ, S::OY))
+      return 1;
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_velocity2d_h<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V::bytes);
+    if (attr != cudaSuccess) return cuda_status(attr);
+    k_velocity2d_h<R><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, V::bytes, s>>>(
+        a, tp, mI, mZ, a.vtmp);
+    int rc = cuda_status(cudaGetLastError());
+    if (rc) return rc;
+    return fir_axis0_r<T, R, false, 1>(tp, a.vtmp, a.v, 2 * g.B, g.H, (long long)g.W, a.guard,
+                                       a.guard_stride, 2, s);
+  }
+}
+
 template <typename T, int R>
 int velocity_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
+  {
+    int rc = velocity_split_r<T, R>(g, tp, a, s);
+    if (rc != 1) return rc;
+  }
   {
     int rc = velocity_stream_r<T, R>(g, tp, a, s);
     if (rc != 1) return rc;
@@ -114,7 +149,7 @@ int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStre
 
 template <typename T, int R, bool TR, int EPI>
 int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                int32_t* guard, int guard_stride, cudaStream_t s);
+                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s);
 
 // Split velocity adjoint (fp32, scratch given): whole-column axis-0 transposed FIR
 // into a.vtmp (k_fir_axis0_f32), then the axis-1 pass + epilogue
@@ -135,7 +170,7 @@ int veladj_split_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStrea
                     make_map3<T>(&m.z, a.z, g.W, g.H, g.B, V::OXP, S::OY);
     if (!ok) return 1;
     int rc = fir_axis0_r<T, R, true, 0>(tp, a.vbar, a.vtmp, (int)B2, g.H, (long long)g.W, nullptr,
-                                        0, s);
+                                        0, 2, s);
     if (rc) return rc;
     constexpr size_t bytes = V::bytes;
     static const cudaError_t attr = cudaFuncSetAttribute(
@@ -179,8 +214,8 @@ int veladj_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s)
 
 template <typename T>
 int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
-                      int32_t* guard, int guard_stride, cudaStream_t s) {
-  VelArgs<T> a{I, z, v, guard, guard_stride, 0, g};
+                      int32_t* guard, int guard_stride, cudaStream_t s, T* vtmp) {
+  VelArgs<T> a{I, z, v, guard, guard_stride, 0, g, vtmp};
   switch (R) {
 #define MR_CASE(RR) \
   case RR: return velocity_r<T, RR>(g, tp, a, s);
@@ -219,7 +254,7 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
 
 template <typename T, int R, bool TR, int EPI>
 int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                int32_t* guard, int guard_stride, cudaStream_t s) {
+                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {  // fp32: FFMA2 engine, 64 x 64 tiles
     constexpr size_t bytes = Ax0F32Smem<R>::bytes;
     static const cudaError_t attr = cudaFuncSetAttribute(
@@ -227,7 +262,7 @@ int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long 
     if (attr != cudaSuccess) return cuda_status(attr);
     dim3 grid((unsigned)((HW + kA0X - 1) / kA0X), (unsigned)((D + kA0D - 1) / kA0D), (unsigned)V);
     k_fir_axis0_f32<R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
-                                                               tp);
+                                                               ncomp, tp);
     return cuda_status(cudaGetLastError());
   } else {
   constexpr size_t bytes = Ax0Smem<T, R>::bytes;
@@ -237,21 +272,22 @@ int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long 
   dim3 grid((unsigned)((HW + kAx0X - 1) / kAx0X), (unsigned)((D + kAx0D - 1) / kAx0D),
             (unsigned)V);
   k_fir_axis0<T, R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
-                                                            tp);
+                                                            ncomp, tp);
   return cuda_status(cudaGetLastError());
   }
 }
 
 template <typename T>
 int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                     bool transpose, int epi, int32_t* guard, int guard_stride, cudaStream_t s) {
+                     bool transpose, int epi, int32_t* guard, int guard_stride, int ncomp,
+                     cudaStream_t s) {
   switch (R) {
 #define MR_CASE(RR)                                                                          \
   case RR:                                                                                   \
     if (transpose)                                                                           \
-      return fir_axis0_r<T, RR, true, 0>(tp, in, out, V, D, HW, guard, guard_stride, s);     \
-    if (epi) return fir_axis0_r<T, RR, false, 1>(tp, in, out, V, D, HW, guard, guard_stride, s); \
-    return fir_axis0_r<T, RR, false, 0>(tp, in, out, V, D, HW, guard, guard_stride, s);
+      return fir_axis0_r<T, RR, true, 0>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s);     \
+    if (epi) return fir_axis0_r<T, RR, false, 1>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s); \
+    return fir_axis0_r<T, RR, false, 0>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s);
     MR_RADIUS_LIST(MR_CASE)
 #undef MR_CASE
     default: return MR_EINVAL;
@@ -265,7 +301,7 @@ int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D
 #define MR_INSTANTIATE_VELOCITY(T)                                                              \
   namespace mr {                                                                                \
   template int launch_velocity2d<T>(const Grid2&, int, const Taps<T>&, const T*, const T*, T*,  \
-                                    int32_t*, int, cudaStream_t);                               \
+                                    int32_t*, int, cudaStream_t, T*);                           \
   }
 #define MR_INSTANTIATE_SMOOTH(T)                                                                \
   namespace mr {                                                                                \
@@ -280,7 +316,7 @@ int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D
 #define MR_INSTANTIATE_AXIS0(T)                                                                 \
   namespace mr {                                                                                \
   template int launch_fir_axis0<T>(int, const Taps<T>&, const T*, T*, int, int, long long, bool, \
-                                   int, int32_t*, int, cudaStream_t);                           \
+                                   int, int32_t*, int, int, cudaStream_t);                      \
   }
 
 // Radius groups: the per-radius kernels of the two heavy launchers (velocity,

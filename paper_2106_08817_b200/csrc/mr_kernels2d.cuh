@@ -360,6 +360,7 @@ struct VelArgs {
   int guard_stride;
   int use_tma;        // tensor maps valid (else cp.async staging)
   Grid2 g;
+  T* vtmp;            // nullable [B][2][N] scratch: enables the split (two-kernel) path
 };
 
 // smem of K1: mbarrier | region m[2][RY][PX] (z staged into m[1]) |
@@ -1320,6 +1321,125 @@ __global__ void __launch_bounds__(kThreads)
   if (REG) {
     unsigned all = __reduce_or_sync(0xffffffffu, bad);
     if (all && lane == 0) atomicOr(reinterpret_cast<int*>(a.flags + b), 1);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// K1 split path, first kernel (fp32): m = z grad I (gradient_arr, fields.py:161-162)
+// fused with the axis-1 pass of smooth_vec_arr (kernel.py:82-85, axis 1 first).
+// TMA stages I (rows y_org-1 .. y_org+OY, cols x_org-R-1 .. x_org+OX+R) and z
+// (rows y_org .. y_org+OY-1, cols x_org-R .. x_org+OX+R-1); the product is formed
+// at the CLAMPED column (replicate border of conv1d_replicate, kernel.py:43-44),
+// whose stencil always lies inside the staged box, straight into the odd-pitch
+// pass-2 buffer; fir2d_pass2 filters the rows and the tile goes to `out`
+// [B][2][H][W].  k_fir_axis0_f32<R, false, 1> then runs the axis-0 pass over
+// whole columns (negate + velocity guard).  FIR work 2(2R+1) FFMA per pixel.
+// ------------------------------------------------------------------------------
+template <int R>
+struct VelHSmem {
+  using S = FirSmem<float, R, 2>;
+  static constexpr int OY = S::OY, RX = S::RX;
+  static constexpr int PXI = round_up(RX + 2 + S::A - 1, S::A);  // I box width
+  static constexpr int PXZ = round_up(RX + S::A - 1, S::A);      // z box width
+  static constexpr int IS = round_up((OY + 2) * PXI, 32);
+  static constexpr int ZS = round_up(OY * PXZ, 32);
+  static constexpr int resn = round_up(2 * OY * S::OP, 32);
+  static constexpr int rg = IS + ZS > resn ? IS + ZS : resn;
+  static constexpr size_t head = 128;
+  static constexpr size_t bytes = head + sizeof(float) * (size_t)(rg + S::vt);
+};
+
+template <int R>
+__global__ void __launch_bounds__(kThreads)
+    k_velocity2d_h(VelArgs<float> a, Taps<float> tp, const __grid_constant__ CUtensorMap mI,
+                   const __grid_constant__ CUtensorMap mZ, float* __restrict__ out) {
+  using T = float;
+  using S = FirSmem<T, R, 2>;
+  using V = VelHSmem<R>;
+  constexpr int OX = S::OX, OY = S::OY, OP = S::OP, RX = S::RX, VP = S::VP, PXI = V::PXI,
+                PXZ = V::PXZ;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  T* rg0 = reinterpret_cast<T*>(smem_raw + V::head);
+  T* sI = rg0;
+  T* sZ = rg0 + V::IS;
+  T* vt = rg0 + V::rg;
+  T* res = rg0;  // [2][OY][OP] once the product is formed
+  const int H = a.g.H, W = a.g.W;
+  const long long N = a.g.N;
+  const int b = blockIdx.z;
+  const int x_org = blockIdx.x * OX, y_org = blockIdx.y * OY;
+  const int xi = x_org - R - 1, xz = x_org - R;
+  const int xi0 = xi - align_shift(xi, S::A), xz0 = xz - align_shift(xz, S::A);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(bar, (unsigned)(sizeof(T) * (PXI * (OY + 2) + PXZ * OY)));
+    tma_load_3d(sI, &mI, xi0, y_org - 1, b, bar);
+    tma_load_3d(sZ, &mZ, xz0, y_org, b, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // region column i <-> image column x_org - R + i, evaluated at its clamped column
+  // (warp <-> row, lanes <-> consecutive columns: conflict-free smem on both sides)
+  const int warp = tid >> 5, lane = tid & 31;
+  const bool interior = x_org - R >= 1 && x_org + OX + R <= W - 1 && y_org >= 1 &&
+                        y_org + OY <= H - 1;
+  if (interior) {  // no clamps, central differences everywhere
+#pragma unroll
+    for (int r = warp; r < OY; r += kNW) {
+      const T* pI = sI + (r + 1) * PXI + (x_org - R - xi0);
+      const T* pZ = sZ + r * PXZ + (x_org - R - xz0);
+#pragma unroll
+      for (int i = lane; i < RX; i += 32) {
+        const T g0 = (pI[i + PXI] - pI[i - PXI]) * T(0.5);
+        const T g1 = (pI[i + 1] - pI[i - 1]) * T(0.5);
+        const T zz = pZ[i];
+        vt[r * VP + i] = zz * g0;
+        vt[(OY + r) * VP + i] = zz * g1;
+      }
+    }
+  } else {
+    for (int r = warp; r < OY; r += kNW) {
+      const int gy = y_org + r;
+#pragma unroll
+      for (int i = lane; i < RX; i += 32) {
+        T m0 = T(0), m1 = T(0);
+        if (gy < H) {
+          const int gx = min(max(x_org - R + i, 0), W - 1);
+          const T* pI = sI + (r + 1) * PXI + (gx - xi0);
+          const T c = pI[0];
+          const T g0 = grad1(pI[-PXI], c, pI[PXI], gy, H);
+          const T g1 = grad1(pI[-1], c, pI[1], gx, W);
+          const T zz = sZ[r * PXZ + (gx - xz0)];
+          m0 = zz * g0;
+          m1 = zz * g1;
+        }
+        vt[r * VP + i] = m0;
+        vt[(OY + r) * VP + i] = m1;
+      }
+    }
+  }
+  __syncthreads();
+  fir2d_pass2<T, R, 2, false>(vt, res, tp, x_org, W);
+  __syncthreads();
+  T* __restrict__ o = out + (long long)b * 2 * N + (long long)y_org * W + x_org;
+  if (interior || (x_org + OX <= W && y_org + OY <= H)) {
+#pragma unroll
+    for (int rc = warp; rc < 2 * OY; rc += kNW) {
+      const int c = rc / OY, r = rc - c * OY;
+#pragma unroll
+      for (int i = lane; i < OX; i += 32) o[c * N + (long long)r * W + i] = res[rc * OP + i];
+    }
+  } else {
+    for (int rc = warp; rc < 2 * OY; rc += kNW) {
+      const int c = rc / OY, r = rc - c * OY;
+      if (y_org + r >= H) continue;
+#pragma unroll
+      for (int i = lane; i < OX; i += 32)
+        if (x_org + i < W) o[c * N + (long long)r * W + i] = res[rc * OP + i];
+    }
   }
 }
 

@@ -99,7 +99,7 @@ struct Ax0Smem {
 template <typename T, int R, bool TRANSPOSE, int EPI>
 __global__ void __launch_bounds__(kThreads)
     k_fir_axis0(const T* __restrict__ in, T* out, int D, long long HW, int32_t* guard,
-                int guard_stride, Taps<T> tp) {
+                int guard_stride, int ncomp, Taps<T> tp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* rg = reinterpret_cast<T*>(smem_raw);
   constexpr int RD = kAx0D + 2 * R;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   if (EPI == 1 && guard && flags)
-    atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / 3) * guard_stride), (int)flags);
+    atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / ncomp) * guard_stride), (int)flags);
 }
 
 // 16-byte cp.async with zero fill (src-size 0 when !valid; gmem must stay a valid address)
@@ -209,7 +209,7 @@ struct Ax0F32Smem {
 template <int R, bool TRANSPOSE, int EPI>
 __global__ void __launch_bounds__(kThreads)
     k_fir_axis0_f32(const float* __restrict__ in, float* out, int D, long long HW,
-                    int32_t* guard, int guard_stride, Taps<float> tp) {
+                    int32_t* guard, int guard_stride, int ncomp, Taps<float> tp) {
   static_assert(kA0D == kNW * kRB && kA0X == 64, "one row block per warp, a column pair per lane");
   extern __shared__ __align__(128) float rgf[];  // [RD][kA0X]
   constexpr int RD = Ax0F32Smem<R>::RD;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (EPI == 1 && guard && flags)
-    atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / 3) * guard_stride), (int)flags);
+    atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / ncomp) * guard_stride), (int)flags);
 }
 
 // ------------------------------------------------------------------------------

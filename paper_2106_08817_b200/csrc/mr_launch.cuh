@@ -20,7 +20,7 @@ inline int cuda_status(cudaError_t e) {
 
 template <typename T>
 int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
-                      int32_t* guard, int guard_stride, cudaStream_t s);
+                      int32_t* guard, int guard_stride, cudaStream_t s, T* vtmp = nullptr);
 template <typename T>
 int launch_smooth2d(const Grid2& g, int R, const Taps<T>& tp, const T* a, T* out, bool transpose,
                     cudaStream_t s);
@@ -29,9 +29,10 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
                           bool reg, cudaStream_t s);
 
 // 1D FIR along axis 0 of V volumes [V][D][HW] (3D velocity / its adjoint);
-// epi = 1: negate + velocity guard (guard word of pair vol/3).
+// epi = 1: negate + velocity guard (guard word of pair vol/ncomp).
 template <typename T>
 int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                     bool transpose, int epi, int32_t* guard, int guard_stride, cudaStream_t s);
+                     bool transpose, int epi, int32_t* guard, int guard_stride, int ncomp,
+                     cudaStream_t s);
 
 }  // namespace mr

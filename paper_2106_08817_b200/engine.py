@@ -178,8 +178,19 @@ def cost_terms(I0, z0, v0, IT, J, lam, rho, stream=None) -> torch.Tensor:
     return terms
 
 
-def velocity(I: torch.Tensor, z: torch.Tensor, weights, guard=None, stream=None) -> torch.Tensor:
-    """v = -K*(z grad I) for a batch [B, *shape] -> [B, d, *shape] (integrator.py:93-94)."""
+def _split_workspace(I: torch.Tensor, split: bool):
+    """2 scalars per pixel of scratch for the split (two-kernel) 2D FIR paths."""
+    if not split or I.dim() != 3:
+        return None
+    return torch.empty((I.shape[0], 2) + tuple(I.shape[1:]), dtype=I.dtype, device=I.device)
+
+
+def velocity(I: torch.Tensor, z: torch.Tensor, weights, guard=None, stream=None,
+             split: bool = True) -> torch.Tensor:
+    """v = -K*(z grad I) for a batch [B, *shape] -> [B, d, *shape] (integrator.py:93-94).
+
+    split=True passes a workspace so the fp32 path runs the same two kernels as
+    mr_shoot_forward; split=False runs the single-kernel variant."""
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
@@ -188,7 +199,7 @@ def velocity(I: torch.Tensor, z: torch.Tensor, weights, guard=None, stream=None)
     kern = _lib.KernelHandle(weights)
     rc = lib.mr_velocity(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), kern.struct,
                          _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(guard),
-                         _lib.stream_ptr(stream))
+                         _lib.ptr(_split_workspace(I, split)), _lib.stream_ptr(stream))
     _lib.check(rc)
     return v
 
@@ -224,15 +235,18 @@ def sl_step_adjoint(I, z, v, ibar, zbar, dt, mu, stream=None):
     return ib, zb, vbar
 
 
-def velocity_adjoint(I, z, vbar, ib, zb, weights, stream=None):
-    """In place: zb += mbar.grad I, ib += G^T(mbar z), mbar = -K^T vbar (objective.py:157-161)."""
+def velocity_adjoint(I, z, vbar, ib, zb, weights, stream=None, split: bool = True):
+    """In place: zb += mbar.grad I, ib += G^T(mbar z), mbar = -K^T vbar (objective.py:157-161).
+
+    split as in velocity(): True runs the kernels mr_shoot_adjoint runs."""
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
     kern = _lib.KernelHandle(weights)
     rc = lib.mr_velocity_adjoint(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), kern.struct,
                                  _lib.ptr(I), _lib.ptr(z), _lib.ptr(vbar), _lib.ptr(ib),
-                                 _lib.ptr(zb), _lib.stream_ptr(stream))
+                                 _lib.ptr(zb), _lib.ptr(_split_workspace(I, split)),
+                                 _lib.stream_ptr(stream))
     _lib.check(rc)
     return ib, zb
 

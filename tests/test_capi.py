@@ -42,7 +42,8 @@ def test_library_rejects_bad_arguments_without_gpu():
 
     lib = _lib.load_library(require_cuda=False)
     g = _lib.make_grid(1, (1, 5))
-    rc = lib.mr_velocity(0, g, _lib.KernelHandle(np.ones(3) / 3).struct, None, None, None, None, None)
+    rc = lib.mr_velocity(0, g, _lib.KernelHandle(np.ones(3) / 3).struct, None, None, None, None, None,
+                         None)
     assert rc == 1
     assert b"at least 2x2" in lib.mr_last_error()
     g = _lib.make_grid(1, (8, 8))

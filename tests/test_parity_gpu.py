@@ -360,3 +360,33 @@ def test_host_pipeline_matches_device_call(chunks):
     for b in (0, B - 1):
         g = O.grad(src[b], tgt[b], z0[b], lam, rho, T, mu, w)
         assert rel_l2(zb_h[b], g) < 1e-3
+
+
+@pytest.mark.parametrize("split", [True, False], ids=["split", "single"])
+@pytest.mark.parametrize("B,H,W,R", [(1, 40, 56, 3), (2, 97, 152, 12), (3, 64, 128, 24),
+                                     (1, 20, 24, 24), (2, 130, 200, 9)])
+def test_velocity_operators_match_oracle(B, H, W, R, split):
+    """mr_velocity / mr_velocity_adjoint, both kernel structures (split = product +
+    axis-1 tile pass, then whole-column axis-0 pass) against the oracle:
+    v = -K(z grad I) (integrator.py:93-94) and its adjoint (objective.py:157-161)."""
+    from oracle import morphreg_oracle as O
+
+    eng = _eng()
+    rng = np.random.default_rng(1000 * R + H)
+    w = O.gaussian_weights(R / 3.0, R)
+    I = rng.random((B, H, W))
+    z = rng.standard_normal((B, H, W))
+    vbar = rng.standard_normal((B, 2, H, W))
+    ib0 = rng.standard_normal((B, H, W))
+    zb0 = rng.standard_normal((B, H, W))
+    for dtype, tol in ((torch.float32, 1e-5), (torch.float64, 1e-12)):
+        v = eng.velocity(_dev(I, dtype), _dev(z, dtype), w, split=split).cpu().numpy()
+        ib, zb = _dev(ib0, dtype), _dev(zb0, dtype)
+        eng.velocity_adjoint(_dev(I, dtype), _dev(z, dtype), _dev(vbar, dtype), ib, zb, w,
+                             split=split)
+        for b in range(B):
+            assert rel_l2(v[b], O.velocity(z[b], O.gradient(I[b]), w)) < tol
+            mbar = -np.stack([O.smooth_adjoint(vbar[b, c], w) for c in range(2)])
+            gi = O.gradient(I[b])
+            assert rel_l2(zb[b].cpu().numpy(), zb0[b] + (mbar * gi).sum(0)) < tol
+            assert rel_l2(ib[b].cpu().numpy(), ib0[b] + O.gradient_adjoint(mbar * z[b])) < tol
