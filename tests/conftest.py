@@ -25,6 +25,11 @@ def shoot_cases():
     return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "shoot_*.npz")))
 
 
+def scheme_cases():
+    """Eulerian / Hybrid goldens (tests/golden/make_golden.py SCHEME_CASES)."""
+    return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "scheme_*.npz")))
+
+
 def rel_l2(a, b):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)

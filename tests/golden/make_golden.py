@@ -82,11 +82,26 @@ def cf(v):
     return np.moveaxis(np.asarray(v), -1, 0)
 
 
-def shoot_case(name, shape, seed, T, mu, sigma, radius, amp, lam, rho, full, margin=0.2):
+# Eulerian / Hybrid schemes (integrator.py:97-106, objective.py:124-127,148-155):
+# (name, scheme, shape, seed, T, mu, sigma, radius, amp, lam, rho, full_states)
+SCHEME_CASES = [
+    ("eu_A_16sq", "eulerian", (16, 16), 20, 5, 0.05, 1.0, None, 0.05, 1e-3, 0.5, True),
+    ("eu_B_13x21", "eulerian", (13, 21), 21, 3, 0.5, 1.5, None, 0.3, 1e-2, 1.0, True),
+    ("eu_C_40x36_r12", "eulerian", (40, 36), 22, 4, 0.3, 3.0, 12, 2.0, 1e-3, 1.0, True),
+    ("eu_D_72x100_r24", "eulerian", (72, 100), 23, 4, 0.0, 6.0, 24, 3.0, 1e-4, 1.0, False),
+    ("hy_A_16sq", "hybrid", (16, 16), 24, 5, 0.05, 1.0, None, 0.05, 1e-3, 0.5, True),
+    ("hy_B_24x20", "hybrid", (24, 20), 25, 3, 0.5, 1.5, None, 0.5, 1e-2, 1.0, True),
+    ("hy_C_48sq_bigdisp", "hybrid", (48, 48), 26, 4, 0.1, 2.0, None, 40.0, 1e-3, 1.0, True),
+    ("hy_D_66x90_r9", "hybrid", (66, 90), 27, 4, 0.3, 3.0, 9, 3.0, 1e-2, 1.0, False),
+]
+
+
+def shoot_case(name, shape, seed, T, mu, sigma, radius, amp, lam, rho, full, margin=0.2,
+               scheme=Scheme.SEMI_LAGRANGIAN, prefix="shoot"):
     src, tgt, z0 = instance(shape, seed, amp, margin_frac=margin)
     geom = GridGeometry(*shape)
     kern = GaussianKernel(sigma, radius)
-    cfg = ShootingConfig(Scheme.SEMI_LAGRANGIAN, T, mu, kern)
+    cfg = ShootingConfig(scheme, T, mu, kern)
     prob = RegistrationProblem(ScalarField(geom, src), ScalarField(geom, tgt), lam, rho, cfg)
     zf = ScalarField(geom, z0)
     traj = shoot(prob.source, zf, cfg)
@@ -96,7 +111,7 @@ def shoot_case(name, shape, seed, T, mu, sigma, radius, amp, lam, rho, full, mar
         source=src, target=tgt, z0=z0, n_steps=T, mu=mu, sigma=sigma, radius=kern.radius,
         lam=lam, rho=rho, weights=kern.weights,
         cost=np.array([rep.total, rep.data_term, rep.v_norm, rep.z_norm]), grad=g,
-        phi=cf(traj.deformation.coords),
+        phi=cf(traj.deformation.coords), scheme=np.array(scheme.value),
     )
     if full:
         out["I"] = np.stack([s.image.values for s in traj.states])
@@ -107,7 +122,7 @@ def shoot_case(name, shape, seed, T, mu, sigma, radius, amp, lam, rho, full, mar
             out[f"I{k}"] = traj.states[k].image.values
             out[f"z{k}"] = traj.states[k].momentum.values
             out[f"v{k}"] = cf(traj.states[k].velocity.values)
-    np.savez_compressed(os.path.join(HERE, f"shoot_{name}.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, f"{prefix}_{name}.npz"), **out)
     print(name, "cost", rep.total, "max|grad|", np.abs(g).max(),
           "max disp", np.abs(cf(traj.states[0].velocity.values)).max() / T)
 
@@ -202,4 +217,6 @@ if __name__ == "__main__":
     guard_case()
     for case in SHOOT_CASES:
         shoot_case(*case)
+    for name, scheme, *rest in SCHEME_CASES:
+        shoot_case(name, *rest, scheme=Scheme(scheme), prefix="scheme")
     config1_case()

@@ -9,7 +9,7 @@ differences of the 3D gradient.
 import numpy as np
 import pytest
 
-from conftest import load_golden, rel_l2, shoot_cases
+from conftest import load_golden, rel_l2, scheme_cases, shoot_cases
 from oracle import morphreg_oracle as O
 
 
@@ -36,13 +36,14 @@ def test_ops_match_reference_goldens():
         assert np.array_equal(O.smooth_adjoint(a, w), g[key + "_smoothT"])
 
 
-@pytest.mark.parametrize("case", shoot_cases())
+@pytest.mark.parametrize("case", shoot_cases() + scheme_cases())
 def test_oracle_shoot_cost_grad_match_reference(case):
     g = load_golden(case)
     w = O.gaussian_weights(float(g["sigma"]), int(g["radius"]))
     assert np.array_equal(w, g["weights"])
     T, mu = int(g["n_steps"]), float(g["mu"])
-    I, z, v, phi = O.shoot(g["source"], g["z0"], T, mu, w)
+    scheme = str(g["scheme"])
+    I, z, v, phi = O.shoot(g["source"], g["z0"], T, mu, w, scheme=scheme)
     if "I" in g:
         for k in range(T + 1):
             assert np.array_equal(I[k], g["I"][k]), k
@@ -54,9 +55,11 @@ def test_oracle_shoot_cost_grad_match_reference(case):
             assert np.array_equal(z[k], g[f"z{k}"])
             assert np.array_equal(v[k], g[f"v{k}"])
     assert np.array_equal(phi, g["phi"])
-    c = O.cost(g["source"], g["target"], g["z0"], float(g["lam"]), float(g["rho"]), T, mu, w)
+    c = O.cost(g["source"], g["target"], g["z0"], float(g["lam"]), float(g["rho"]), T, mu, w,
+               scheme=scheme)
     assert np.allclose(c, g["cost"], rtol=1e-14, atol=0)
-    gr = O.grad(g["source"], g["target"], g["z0"], float(g["lam"]), float(g["rho"]), T, mu, w)
+    gr = O.grad(g["source"], g["target"], g["z0"], float(g["lam"]), float(g["rho"]), T, mu, w,
+                scheme=scheme)
     assert rel_l2(gr, g["grad"]) < 1e-13
 
 
