@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", type=int, default=2)
+    p.add_argument("--scheme", default="semi-lagrangian",
+                   choices=["semi-lagrangian", "eulerian", "hybrid"],
+                   help="shooting scheme (2D configs; the hot path is semi-lagrangian)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--e2e-chunks", type=int, default=None,
@@ -155,7 +158,9 @@ def run_ours(args):
     T = c.n_steps
     w = c.weights()
     dtype = torch.float32
-    bg = engine.BatchGrad(len(pairs), c.shape, T, c.mu, w, c.lam, c.rho, dtype)
+    sl = args.scheme == "semi-lagrangian"
+    bg = engine.BatchGrad(len(pairs), c.shape, T, c.mu, w, c.lam, c.rho, dtype,
+                          scheme=args.scheme)
     bg.load(torch.as_tensor(c.source, dtype=dtype), torch.as_tensor(c.target, dtype=dtype),
             torch.as_tensor(c.z0, dtype=dtype))
     stream = torch.cuda.current_stream()
@@ -202,13 +207,13 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     step_bytes = sum(ab.values()) * Bl * N * T
     step_achieved = step_bytes / (ms * 1e-3) / 1e9
-    if d == 2:
+    if d == 2 and sl:
         kt = kernel_times(bg, w, stream)
         launches = {"velocity": T + 1, "sl_step": T, "sl_adjoint": T, "velocity_adjoint": T}
         share = {k: kt[k] * launches[k] / ms for k in kt}
         dom = max(share, key=share.get)
         achieved = ab[dom] * Bl * N / (kt[dom] * 1e-3) / 1e9
-    else:  # 3D sweeps are multi-kernel chains: report the whole step against HBM
+    else:  # 3D / Eulerian / Hybrid: report the whole step against HBM
         kt, share, dom = {}, {"step": 1.0}, "step"
         achieved = step_achieved
         kt["step"] = ms
@@ -231,7 +236,9 @@ def run_ours(args):
         "data": f"synthetic (seeded cfg-{args.config} generator, calibrated z0; SURVEY §8(d))",
         "config": {
             "workload": f"{c.name}: {B_global} pairs x {'x'.join(map(str, c.shape))}, T={T}, "
-                        f"sigma={c.sigma}, r={c.radius}, mu={c.mu}, grad() = shoot + adjoint",
+                        f"sigma={c.sigma}, r={c.radius}, mu={c.mu}, grad() = shoot + adjoint"
+                        + ("" if sl else f", scheme={args.scheme}"),
+            "scheme": args.scheme,
             "momentum_scale": c.manifest.get("momentum_scale"),
             "cuda_graph": not args.no_graph,
             "global_batch": B_global,
@@ -271,7 +278,7 @@ def run_ours(args):
         "mean_cost": float(terms[:, 0].mean()),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(c, w)
+        line["cpu_baseline"] = cpu_baseline_sample(c, w, args.scheme)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -351,7 +358,7 @@ def run_e2e(c, args, dtype, world):
 
     import paper_2106_08817_b200 as mr
 
-    cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, c.n_steps, c.mu,
+    cfg = mr.ShootingConfig(mr.Scheme(args.scheme), c.n_steps, c.mu,
                             mr.GaussianKernel(c.sigma, c.radius))
     src = torch.as_tensor(c.source, dtype=dtype).pin_memory()
     tgt = torch.as_tensor(c.target, dtype=dtype).pin_memory()
@@ -404,18 +411,19 @@ def _oracle_grad_task(args):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import morphreg_oracle as O
 
-    src, tgt, z0, T, mu, lam, rho, w = args
+    src, tgt, z0, T, mu, lam, rho, w = args[:8]
+    scheme = args[8] if len(args) > 8 else "semi-lagrangian"
     t0 = time.perf_counter()
-    O.grad(src, tgt, z0, lam, rho, T, mu, w)
+    O.grad(src, tgt, z0, lam, rho, T, mu, w, scheme=scheme)
     return time.perf_counter() - t0
 
 
-def cpu_baseline_sample(c, w):
+def cpu_baseline_sample(c, w, scheme="semi-lagrangian"):
     """Oracle port on 1 host core, one pair: ~10-30 s of CPU work (2D: full T;
     3D: T truncated to 1 step -- the cost per voxel-step is T-independent)."""
     src, tgt, z0 = c.source[0], c.target[0], c.z0[0]
     T = c.n_steps if len(c.shape) == 2 else 1
-    sec = _oracle_grad_task((src, tgt, z0, T, c.mu, c.lam, c.rho, w))
+    sec = _oracle_grad_task((src, tgt, z0, T, c.mu, c.lam, c.rho, w, scheme))
     vs = int(np.prod(c.shape)) * T
     return {"value": vs / sec, "unit": "voxel-steps/s", "cores": 1, "kind": "port",
             "sample": f"oracle grad() of 1 pair {'x'.join(map(str, c.shape))}, T={T}, "
@@ -437,7 +445,8 @@ def run_reference(args):
     P = min(cores, spec["batch"])
     c = make_config(args.config, batch=P)
     w = c.weights()
-    tasks = [(c.source[i], c.target[i], c.z0[i], T_sample, c.mu, c.lam, c.rho, w) for i in range(P)]
+    tasks = [(c.source[i], c.target[i], c.z0[i], T_sample, c.mu, c.lam, c.rho, w, args.scheme)
+             for i in range(P)]
     Nv = int(np.prod(c.shape))
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:

@@ -55,6 +55,14 @@ enum {
   MR_GUARD_VELOCITY_MAGNITUDE = 1 << 5
 };
 
+/* Shooting scheme (Scheme, integrator.py:48-51).  The Eulerian and Hybrid
+ * schemes are 2D, as in the reference. */
+enum {
+  MR_SCHEME_SEMI_LAGRANGIAN = 0,
+  MR_SCHEME_EULERIAN = 1,
+  MR_SCHEME_HYBRID = 2
+};
+
 /* Grid of a batch of independent pairs (GridGeometry, fields.py:20-38). */
 typedef struct {
   int32_t ndim;   /* 2 or 3 */
@@ -133,6 +141,16 @@ int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu,
                      void* traj_v, void* phi, int32_t* guard, void* workspace,
                      void* stream);
 
+/* shoot() for any Scheme (integrator.py:163-219, branches :194-201): as
+ * mr_shoot_forward (which is scheme = MR_SCHEME_SEMI_LAGRANGIAN).
+ * EULERIAN: I' = I + dt(-(grad I . v) + mu z), z' = z - dt div(z v);
+ * HYBRID:   I' = B(I) + dt mu z,               z' = z - dt div(z v);
+ * both warp phi with the bilinear plan. */
+int mr_shoot_forward_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme,
+                            double mu, int32_t n_steps, void* traj_I,
+                            void* traj_z, void* traj_v, void* phi,
+                            int32_t* guard, void* workspace, void* stream);
+
 /* Bytes of device workspace mr_shoot_adjoint needs for grid g. */
 size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g);
 
@@ -148,6 +166,16 @@ int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu,
                      const void* traj_v, const void* J, void* zbar0,
                      double* terms, int32_t* flags, void* workspace,
                      void* stream);
+
+/* grad() for any Scheme (objective.py:91-174, branches :124-155) over a
+ * trajectory from mr_shoot_forward_scheme with the same scheme; arguments as
+ * mr_shoot_adjoint (which is scheme = MR_SCHEME_SEMI_LAGRANGIAN). */
+int mr_shoot_adjoint_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme,
+                            double mu, int32_t n_steps, double lam, double rho,
+                            const void* traj_I, const void* traj_z,
+                            const void* traj_v, const void* J, void* zbar0,
+                            double* terms, int32_t* flags, void* workspace,
+                            void* stream);
 
 /* cost() terms (objective.py:71-88) from a trajectory's final image and the
  * initial state: terms double[B][4] = {total, data, v_norm, z_norm}.

@@ -22,6 +22,9 @@ MR_F32 = 0
 MR_F64 = 1
 MR_MAX_RADIUS = 32
 
+# Scheme codes (MR_SCHEME_*, include/morphreg_sm100.h) by Scheme value.
+SCHEME_CODES = {"semi-lagrangian": 0, "eulerian": 1, "hybrid": 2}
+
 GUARD_BITS = (
     (1 << 0, "non-finite image"),
     (1 << 1, "image magnitude above guard"),
@@ -38,9 +41,11 @@ EXPORTS = (
     "mr_sl_step_adjoint",
     "mr_velocity_adjoint",
     "mr_shoot_forward",
+    "mr_shoot_forward_scheme",
     "mr_forward_workspace_bytes",
     "mr_adjoint_workspace_bytes",
     "mr_shoot_adjoint",
+    "mr_shoot_adjoint_scheme",
     "mr_cost_terms",
     "mr_smooth",
     "mr_last_error",
@@ -67,11 +72,18 @@ _SIGNATURES = {
     "mr_sl_step_adjoint": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_velocity_adjoint": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_shoot_forward": (_i32, [_i32, MrGrid, MrKernel, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_shoot_forward_scheme": (
+        _i32, [_i32, MrGrid, MrKernel, _i32, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_forward_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
     "mr_adjoint_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
     "mr_shoot_adjoint": (
         _i32,
         [_i32, MrGrid, MrKernel, _d, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    ),
+    "mr_shoot_adjoint_scheme": (
+        _i32,
+        [_i32, MrGrid, MrKernel, _i32, _d, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+         _vp],
     ),
     "mr_cost_terms": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_smooth": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _i32, _vp]),

@@ -14,6 +14,7 @@
 
 #include "mr_launch.cuh"
 #include "mr_tma.h"
+#include "mr_schemes2d.cuh"
 #include "mr_transport2d.cuh"
 
 namespace mr {
@@ -200,6 +201,30 @@ static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I,
   return cuda_status(cudaGetLastError());
 }
 
+// Eulerian / Hybrid transport step and its adjoint (mr_schemes2d.cuh).
+template <typename T>
+static int launch_scheme_step2d(int scheme, const Grid2& g, double dt, double mu, const T* I,
+                                const T* z, const T* v, T* In, T* zn, const T* phi_in,
+                                T* phi_out, cudaStream_t s, int32_t* guard_in,
+                                int32_t* guard_out, int guard_stride) {
+  StepArgs<T> a{I,     z,       v,      In,        zn,          phi_in,
+                phi_out, (T)dt, (T)(dt * mu), mu != 0.0, guard_in, guard_out,
+                guard_stride, g};
+  dim3 grid((g.W + 31) / 32, (g.H + kNW - 1) / kNW, g.B);
+  k_scheme_step2d<T><<<grid, kThreads, 0, s>>>(a, (T)mu, scheme);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_scheme_adj2d(int scheme, const Grid2& g, double dt, double mu, const T* I,
+                               const T* z, const T* v, const T* ibar, const T* zbar, T* ib, T* zb,
+                               T* vbar, cudaStream_t s, double reg_lam) {
+  AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, (T)reg_lam, g};
+  dim3 grid((g.W + 31) / 32, (g.H + kNW - 1) / kNW, g.B);
+  k_scheme_adj2d<T><<<grid, kThreads, 0, s>>>(a, scheme);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T>
 static int launch_cost_terms2d(const Grid2& g, double lam, double rho, const T* I0, const T* z0,
                                const T* v0, const T* IT, const T* J, double* terms, T* seed,
@@ -250,7 +275,7 @@ static int shoot_forward3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
 }
 
 template <typename T>
-static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T_, void* trI,
+static int shoot_forward(const mr_grid& mg, const mr_kernel& k, int scheme, double mu, int T_, void* trI,
                          void* trz, void* trv, void* phi, int32_t* guard, void* ws,
                          cudaStream_t s) {
   Taps<T> tp;
@@ -285,11 +310,18 @@ static int shoot_forward(const mr_grid& mg, const mr_kernel& k, double mu, int T
     rc = launch_velocity2d<T>(g, k.radius, tp, I + step * S1, z + step * S1, v + step * SV,
                               guard ? guard + step : nullptr, T_ + 1, s, static_cast<T*>(ws));
     if (rc) return check_rc(rc, "velocity");
-    rc = launch_sl_step2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV,
-                             I + (step + 1) * S1, z + (step + 1) * S1, ph[step & 1],
-                             ph[(step + 1) & 1], s,
-                             (guard && step == 0) ? guard : nullptr,
-                             guard ? guard + step + 1 : nullptr, T_ + 1);
+    if (scheme == kSchemeSL)
+      rc = launch_sl_step2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV,
+                               I + (step + 1) * S1, z + (step + 1) * S1, ph[step & 1],
+                               ph[(step + 1) & 1], s,
+                               (guard && step == 0) ? guard : nullptr,
+                               guard ? guard + step + 1 : nullptr, T_ + 1);
+    else
+      rc = launch_scheme_step2d<T>(scheme, g, dt, mu, I + step * S1, z + step * S1,
+                                   v + step * SV, I + (step + 1) * S1, z + (step + 1) * S1,
+                                   ph[step & 1], ph[(step + 1) & 1], s,
+                                   (guard && step == 0) ? guard : nullptr,
+                                   guard ? guard + step + 1 : nullptr, T_ + 1);
     if (rc) return check_rc(rc, "sl_step");
   }
   rc = launch_velocity2d<T>(g, k.radius, tp, I + T_ * S1, z + T_ * S1, v + T_ * SV,
@@ -383,7 +415,7 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
 }
 
 template <typename T>
-static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T_, double lam,
+static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, int scheme, double mu, int T_, double lam,
                          double rho, const void* trI, const void* trz, const void* trv,
                          const void* Jv, void* zbar0, double* terms, int32_t* flags, void* ws,
                          cudaStream_t s) {
@@ -418,8 +450,13 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, double mu, int T
   if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
   if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
   for (int step = T_ - 1; step >= 0; --step) {
-    rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
-                                cur + S1, acc, acc + S1, vbar, s, step == 0 ? lam : 0.0);
+    if (scheme == kSchemeSL)
+      rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
+                                  cur + S1, acc, acc + S1, vbar, s, step == 0 ? lam : 0.0);
+    else
+      rc = launch_scheme_adj2d<T>(scheme, g, dt, mu, I + step * S1, z + step * S1,
+                                  v + step * SV, cur, cur + S1, acc, acc + S1, vbar, s,
+                                  step == 0 ? lam : 0.0);
     if (rc) return check_rc(rc, "sl_adjoint");
     VelAdjArgs<T> a{};
     a.I = I + step * S1;
@@ -596,18 +633,35 @@ size_t mr_forward_workspace_bytes(int dtype, mr_grid g) {
   return (size_t)(dtype == MR_F32 ? 4 : 8) * (size_t)scalars(g) * (g.ndim == 2 ? 2 : 3);
 }
 
+static int validate_scheme(int32_t scheme, const mr_grid& g) {
+  if (scheme != MR_SCHEME_SEMI_LAGRANGIAN && scheme != MR_SCHEME_EULERIAN &&
+      scheme != MR_SCHEME_HYBRID)
+    return fail(MR_EINVAL, "unknown scheme " + std::to_string(scheme));
+  if (scheme != MR_SCHEME_SEMI_LAGRANGIAN && g.ndim != 2)
+    return fail(MR_EINVAL, "the eulerian and hybrid schemes are 2D (as the reference)");
+  return MR_OK;
+}
+
 int mr_shoot_forward(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps,
                      void* traj_I, void* traj_z, void* traj_v, void* phi, int32_t* guard,
                      void* workspace, void* stream) {
+  return mr_shoot_forward_scheme(dtype, g, k, MR_SCHEME_SEMI_LAGRANGIAN, mu, n_steps, traj_I,
+                                 traj_z, traj_v, phi, guard, workspace, stream);
+}
+
+int mr_shoot_forward_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme, double mu,
+                            int32_t n_steps, void* traj_I, void* traj_z, void* traj_v, void* phi,
+                            int32_t* guard, void* workspace, void* stream) {
   int rc = validate(dtype, g);
   if (rc) return rc;
+  if ((rc = validate_scheme(scheme, g))) return rc;
   if (n_steps < 1) return fail(MR_EINVAL, "n_steps must be >= 1, got " + std::to_string(n_steps));
   if (!(mu >= 0.0)) return fail(MR_EINVAL, "mu must be >= 0");
   if (!traj_I || !traj_z || !traj_v) return fail(MR_EINVAL, "NULL trajectory pointer");
   rc = MR_DISPATCH(dtype,
-                   shoot_forward<float>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
+                   shoot_forward<float>(g, k, scheme, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
                                         workspace, as_stream(stream)),
-                   shoot_forward<double>(g, k, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
+                   shoot_forward<double>(g, k, scheme, mu, n_steps, traj_I, traj_z, traj_v, phi, guard,
                                          workspace, as_stream(stream)));
   if (rc) return rc;
   return check_cuda("mr_shoot_forward");
@@ -624,17 +678,27 @@ int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_ste
                      double rho, const void* traj_I, const void* traj_z, const void* traj_v,
                      const void* J, void* zbar0, double* terms, int32_t* flags, void* workspace,
                      void* stream) {
+  return mr_shoot_adjoint_scheme(dtype, g, k, MR_SCHEME_SEMI_LAGRANGIAN, mu, n_steps, lam, rho,
+                                 traj_I, traj_z, traj_v, J, zbar0, terms, flags, workspace,
+                                 stream);
+}
+
+int mr_shoot_adjoint_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme, double mu,
+                            int32_t n_steps, double lam, double rho, const void* traj_I,
+                            const void* traj_z, const void* traj_v, const void* J, void* zbar0,
+                            double* terms, int32_t* flags, void* workspace, void* stream) {
   int rc = validate(dtype, g);
   if (rc) return rc;
+  if ((rc = validate_scheme(scheme, g))) return rc;
   if (n_steps < 1) return fail(MR_EINVAL, "n_steps must be >= 1");
   if (!(lam > 0.0)) return fail(MR_EINVAL, "lambda must be positive");
   if (!(rho >= 0.0)) return fail(MR_EINVAL, "rho must be >= 0");
   if (!traj_I || !traj_z || !traj_v || !J || !zbar0 || !terms || !flags || !workspace)
     return fail(MR_EINVAL, "NULL pointer");
   rc = MR_DISPATCH(dtype,
-                   shoot_adjoint<float>(g, k, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
+                   shoot_adjoint<float>(g, k, scheme, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
                                         zbar0, terms, flags, workspace, as_stream(stream)),
-                   shoot_adjoint<double>(g, k, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
+                   shoot_adjoint<double>(g, k, scheme, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
                                          zbar0, terms, flags, workspace, as_stream(stream)));
   if (rc) return rc;
   return check_cuda("mr_shoot_adjoint");

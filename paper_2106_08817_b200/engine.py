@@ -75,18 +75,21 @@ def allocate_trajectory(batch, shape, n_steps, dtype=torch.float32, device=None,
     return DeviceTrajectory(I, z, v, guard, phi, ws)
 
 
-def shoot_forward(traj: DeviceTrajectory, mu: float, weights, stream=None) -> DeviceTrajectory:
+def shoot_forward(traj: DeviceTrajectory, mu: float, weights, stream=None,
+                  scheme: str = "semi-lagrangian") -> DeviceTrajectory:
     """Run the forward sweep in place; traj.I[0], traj.z[0] hold I0, z0.
 
-    Launches 2T+1 kernels (+1 identity init with phi) through mr_shoot_forward.
-    Does not synchronise; call :func:`raise_on_guard` to surface divergence.
+    One mr_shoot_forward_scheme call (scheme = a Scheme value) launches the
+    whole sweep.  Does not synchronise; call :func:`raise_on_guard` to surface
+    divergence.
     """
     lib = _lib.load_library()
     kern = _lib.KernelHandle(weights)
     dt = _lib.dtype_code(traj.I.dtype)
     g = _lib.make_grid(traj.batch, traj.shape)
-    rc = lib.mr_shoot_forward(
-        dt, g, kern.struct, float(mu), int(traj.n_steps), _lib.ptr(traj.I), _lib.ptr(traj.z),
+    rc = lib.mr_shoot_forward_scheme(
+        dt, g, kern.struct, _lib.SCHEME_CODES[str(scheme)], float(mu), int(traj.n_steps),
+        _lib.ptr(traj.I), _lib.ptr(traj.z),
         _lib.ptr(traj.v), _lib.ptr(traj.phi), _lib.ptr(traj.guard), _lib.ptr(traj.workspace),
         _lib.stream_ptr(stream),
     )
@@ -141,7 +144,8 @@ class AdjointBuffers:
 
 
 def shoot_adjoint(traj: DeviceTrajectory, target: torch.Tensor, lam: float, rho: float, mu: float,
-                  weights, bufs: AdjointBuffers | None = None, stream=None) -> AdjointBuffers:
+                  weights, bufs: AdjointBuffers | None = None, stream=None,
+                  scheme: str = "semi-lagrangian") -> AdjointBuffers:
     """Reverse sweep of grad() (objective.py:91-174) over a forward trajectory.
 
     Returns the buffers: .zbar = dH/dz0 [B, *shape], .terms = CostReport rows
@@ -153,8 +157,9 @@ def shoot_adjoint(traj: DeviceTrajectory, target: torch.Tensor, lam: float, rho:
         bufs = AdjointBuffers(traj.batch, traj.shape, traj.I.dtype, traj.I.device)
     kern = _lib.KernelHandle(weights)
     g = _lib.make_grid(traj.batch, traj.shape)
-    rc = lib.mr_shoot_adjoint(
-        _lib.dtype_code(traj.I.dtype), g, kern.struct, float(mu), int(traj.n_steps), float(lam),
+    rc = lib.mr_shoot_adjoint_scheme(
+        _lib.dtype_code(traj.I.dtype), g, kern.struct, _lib.SCHEME_CODES[str(scheme)], float(mu),
+        int(traj.n_steps), float(lam),
         float(rho), _lib.ptr(traj.I), _lib.ptr(traj.z), _lib.ptr(traj.v), _lib.ptr(target),
         _lib.ptr(bufs.zbar), _lib.ptr(bufs.terms), _lib.ptr(bufs.flags), _lib.ptr(bufs.workspace),
         _lib.stream_ptr(stream),
@@ -273,7 +278,8 @@ class BatchGrad:
     """
 
     def __init__(self, batch, shape, n_steps, mu, weights, lam, rho, dtype=torch.float32,
-                 device=None):
+                 device=None, scheme: str = "semi-lagrangian"):
+        self.scheme = str(scheme)
         self.traj = allocate_trajectory(batch, shape, n_steps, dtype, device)
         self.target = torch.empty((batch,) + tuple(shape), dtype=dtype,
                                   device=self.traj.I.device)
@@ -288,9 +294,9 @@ class BatchGrad:
         self.target.copy_(target)
 
     def run(self, stream=None):
-        shoot_forward(self.traj, self.mu, self.weights, stream)
+        shoot_forward(self.traj, self.mu, self.weights, stream, scheme=self.scheme)
         shoot_adjoint(self.traj, self.target, self.lam, self.rho, self.mu, self.weights,
-                      self.bufs, stream)
+                      self.bufs, stream, scheme=self.scheme)
         return self.bufs
 
     def capture_graph(self):
@@ -315,7 +321,15 @@ class BatchGrad:
     def launches_per_run(self) -> int:
         """Kernels of ours per run() (memsets excluded)."""
         T = self.n_steps
-        if len(self.traj.shape) == 2:  # forward 2T+1; adjoint cost+finalize + 2T
-            return (2 * T + 1) + (2 + 2 * T)
+        if len(self.traj.shape) == 2:
+            H, W = self.traj.shape
+            f32 = self.traj.I.dtype == torch.float32 and W % 4 == 0
+            # forward: T+1 velocities (2 kernels when split: 64x32 tiles fill the GPU
+            # twice, mr_capi.cu shoot_forward) + T steps; adjoint: cost + finalize +
+            # T x (transport adjoint + velocity adjoint, 2 kernels when split)
+            tiles = ((W + 63) // 64) * ((H + 31) // 32) * self.traj.batch
+            vel = 2 if f32 and tiles >= 2 * 148 else 1
+            vadj = 2 if f32 else 1
+            return (vel * (T + 1) + T) + (2 + (1 + vadj) * T)
         # 3D: velocity = 3 kernels, step 1; adjoint: 2 + (2 + 2 FIR + 1) per step
         return (3 * (T + 1) + T) + (2 + 5 * T)

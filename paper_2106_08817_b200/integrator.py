@@ -1,11 +1,11 @@
 """Geodesic shooting with the reference's signatures (integrator.py:48-219).
 
-``shoot(i0, z0, cfg)`` runs the whole T-step semi-Lagrangian loop on the device
-through one ``mr_shoot_forward`` call (2T+1 kernels), then checks the device
-guard once and raises ``IntegrationDiverged(step, what)`` with the reference's
-text (integrator.py:113-118).  Only ``Scheme.SEMI_LAGRANGIAN`` is accelerated
-in this build; the Eulerian / hybrid schemes are the next rows of the scope
-table and raise ``NotImplementedError``.
+``shoot(i0, z0, cfg)`` runs the whole T-step loop on the device through one
+``mr_shoot_forward_scheme`` call, then checks the device guard once and raises
+``IntegrationDiverged(step, what)`` with the reference's text
+(integrator.py:113-118).  All three schemes run on the device: the
+semi-Lagrangian hot path (TMA-staged kernels, 2D and 3D) and the Eulerian /
+Hybrid stencil steps (integrator.py:97-106, 2D as in the reference).
 """
 
 from __future__ import annotations
@@ -82,14 +82,6 @@ class GeodesicTrajectory:
         return self.states[-1].image
 
 
-def _require_sl(cfg: ShootingConfig) -> None:
-    if cfg.scheme is not Scheme.SEMI_LAGRANGIAN:
-        raise NotImplementedError(
-            f"scheme {cfg.scheme.value!r} is not accelerated in this build "
-            "(semi-lagrangian only; see SURVEY.md §8(f))"
-        )
-
-
 def _to_device(f, dtype) -> torch.Tensor:
     dev = torch.device("cuda", torch.cuda.current_device())
     return f.tensor.to(dev, dtype).contiguous()
@@ -109,12 +101,11 @@ def velocity_from_momentum(z: ScalarField, image: ScalarField, kernel: GaussianK
 def _run(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig, mu: float) -> GeodesicTrajectory:
     if i0.geometry != z0.geometry:
         raise FieldError("image/momentum geometry mismatch")
-    _require_sl(cfg)
     geom = i0.geometry
     traj = engine.allocate_trajectory(1, geom.shape, cfg.n_steps, cfg.dtype, with_phi=True)
     traj.I[0, 0].copy_(_to_device(i0, cfg.dtype))
     traj.z[0, 0].copy_(_to_device(z0, cfg.dtype))
-    engine.shoot_forward(traj, mu, cfg.kernel.weights)
+    engine.shoot_forward(traj, mu, cfg.kernel.weights, scheme=cfg.scheme.value)
     engine.raise_on_guard(traj)
     dt = cfg.dt
     states = []

@@ -16,7 +16,7 @@ import torch
 from . import engine
 from .errors import FieldError
 from .fields import ScalarField
-from .integrator import GeodesicTrajectory, ShootingConfig, _require_sl, _to_device
+from .integrator import GeodesicTrajectory, ShootingConfig, _to_device
 
 __all__ = ["RegistrationProblem", "CostReport", "cost", "grad", "ShootingCost", "cost_and_grad_batch"]
 
@@ -57,12 +57,11 @@ def cost(problem: RegistrationProblem, z0: ScalarField,
     if z0.geometry != problem.source.geometry:
         raise FieldError("initial momentum geometry mismatch")
     cfg = problem.cfg
-    _require_sl(cfg)
     if trajectory is None or trajectory.device is None:
         traj = engine.allocate_trajectory(1, z0.geometry.shape, cfg.n_steps, cfg.dtype)
         traj.I[0, 0].copy_(_to_device(problem.source, cfg.dtype))
         traj.z[0, 0].copy_(_to_device(z0, cfg.dtype))
-        engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights)
+        engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
         engine.raise_on_guard(traj)
     else:
         traj = trajectory.device
@@ -77,14 +76,14 @@ def grad(problem: RegistrationProblem, z0: ScalarField) -> ScalarField:
     if z0.geometry != problem.source.geometry:
         raise FieldError("initial momentum geometry mismatch")
     cfg = problem.cfg
-    _require_sl(cfg)
     traj = engine.allocate_trajectory(1, z0.geometry.shape, cfg.n_steps, cfg.dtype)
     traj.I[0, 0].copy_(_to_device(problem.source, cfg.dtype))
     traj.z[0, 0].copy_(_to_device(z0, cfg.dtype))
-    engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights)
+    engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
     engine.raise_on_guard(traj)
     J = _to_device(problem.target, cfg.dtype).unsqueeze(0)
-    bufs = engine.shoot_adjoint(traj, J, problem.lam, problem.rho, cfg.mu, cfg.kernel.weights)
+    bufs = engine.shoot_adjoint(traj, J, problem.lam, problem.rho, cfg.mu, cfg.kernel.weights,
+                                scheme=cfg.scheme.value)
     if int(bufs.flags[0].item()) != 0:  # objective.py:171-173
         bad = torch.nonzero(~torch.isfinite(bufs.zbar[0]))[0].tolist()
         raise FieldError(f"non-finite gradient entry at pixel {tuple(bad)}")
@@ -101,13 +100,12 @@ class ShootingCost(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, z0, source, target, cfg: ShootingConfig, lam: float, rho: float):
-        _require_sl(cfg)
         B = z0.shape[0]
         shape = tuple(z0.shape[1:])
         traj = engine.allocate_trajectory(B, shape, cfg.n_steps, z0.dtype, z0.device)
         traj.I[0].copy_(source)
         traj.z[0].copy_(z0)
-        engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights)
+        engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
         engine.raise_on_guard(traj)
         tgt = target.contiguous()
         terms = engine.cost_terms(traj.I[0], traj.z[0], traj.v[0], traj.I[-1], tgt, lam, rho)
@@ -119,7 +117,8 @@ class ShootingCost(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad_out):
         cfg, lam, rho = ctx.params
-        bufs = engine.shoot_adjoint(ctx.traj, ctx.target, lam, rho, cfg.mu, cfg.kernel.weights)
+        bufs = engine.shoot_adjoint(ctx.traj, ctx.target, lam, rho, cfg.mu, cfg.kernel.weights,
+                                    scheme=cfg.scheme.value)
         scale = grad_out.to(bufs.zbar.dtype).view((-1,) + (1,) * (bufs.zbar.ndim - 1))
         ctx.traj = None
         return bufs.zbar * scale, None, None, None, None, None
@@ -137,14 +136,14 @@ def cost_and_grad_batch(source: torch.Tensor, target: torch.Tensor, z0: torch.Te
     """
     if not z0.is_cuda:
         return _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunks)
-    _require_sl(cfg)
     B = z0.shape[0]
     shape = tuple(z0.shape[1:])
     traj = engine.allocate_trajectory(B, shape, cfg.n_steps, z0.dtype, z0.device)
     traj.I[0].copy_(source)
     traj.z[0].copy_(z0)
-    engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights)
-    bufs = engine.shoot_adjoint(traj, target.contiguous(), lam, rho, cfg.mu, cfg.kernel.weights)
+    engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
+    bufs = engine.shoot_adjoint(traj, target.contiguous(), lam, rho, cfg.mu, cfg.kernel.weights,
+                                scheme=cfg.scheme.value)
     if raise_on_divergence:
         engine.raise_on_guard(traj)
     return bufs.zbar, bufs.terms, traj.guard
@@ -174,7 +173,6 @@ def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunk
     so the device sees the whole batch; per pair the result is the same as a
     device-tensor call.
     """
-    _require_sl(cfg)
     B = z0.shape[0]
     shape = tuple(z0.shape[1:])
     if tuple(source.shape) != tuple(z0.shape) or tuple(target.shape) != tuple(z0.shape):
@@ -216,9 +214,10 @@ def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunk
         s = streams[g]
         with torch.cuda.stream(s):  # every allocation and launch of group g is on s
             s.wait_event(ev_in[g])
-            engine.shoot_forward(trajs[g], cfg.mu, w, stream=s)
+            engine.shoot_forward(trajs[g], cfg.mu, w, stream=s, scheme=cfg.scheme.value)
             s.wait_event(ev_J[g])
-            bufs = engine.shoot_adjoint(trajs[g], tgts[g], lam, rho, cfg.mu, w, stream=s)
+            bufs = engine.shoot_adjoint(trajs[g], tgts[g], lam, rho, cfg.mu, w, stream=s,
+                                        scheme=cfg.scheme.value)
             keep.append(bufs)
             zbar_h[a:b].copy_(bufs.zbar, non_blocking=True)
             terms_h[a:b].copy_(bufs.terms, non_blocking=True)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import load_golden, rel_l2, shoot_cases
+from conftest import load_golden, rel_l2, scheme_cases, shoot_cases
 
 pytestmark = pytest.mark.gpu
 
@@ -39,10 +39,12 @@ def _fp32_sensitivity(case, g):
     from oracle import morphreg_oracle as O
 
     T, mu = int(g["n_steps"]), float(g["mu"])
+    sch = str(g["scheme"])
     r = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
-    I, z, v, _ = O.shoot(r(g["source"]), r(g["z0"]), T, mu, g["weights"], with_phi=False)
+    I, z, v, _ = O.shoot(r(g["source"]), r(g["z0"]), T, mu, g["weights"], with_phi=False,
+                         scheme=sch)
     gr = O.grad(r(g["source"]), r(g["target"]), r(g["z0"]), float(g["lam"]), float(g["rho"]), T, mu,
-                g["weights"])
+                g["weights"], scheme=sch)
     ref = lambda name, k: g[name][k] if name in g else g[f"{name}{k}"]  # noqa: E731
     steps = range(T + 1) if "I" in g else (0, T)
     s = {k: max(rel_l2(I[k], ref("I", k)), rel_l2(z[k], ref("z", k)), rel_l2(v[k], ref("v", k)))
@@ -60,15 +62,17 @@ def _run_case(g, dtype, batch_copies=1):
     for b in range(batch_copies):
         traj.I[0, b].copy_(_dev(g["source"], dtype))
         traj.z[0, b].copy_(_dev(g["z0"], dtype))
-    eng.shoot_forward(traj, mu, g["weights"])
+    sch = str(g["scheme"])
+    eng.shoot_forward(traj, mu, g["weights"], scheme=sch)
     J = _dev(np.repeat(g["target"][None], batch_copies, 0), dtype)
-    bufs = eng.shoot_adjoint(traj, J, float(g["lam"]), float(g["rho"]), mu, g["weights"])
+    bufs = eng.shoot_adjoint(traj, J, float(g["lam"]), float(g["rho"]), mu, g["weights"],
+                             scheme=sch)
     torch.cuda.synchronize()
     return traj, bufs
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64], ids=["fp32", "fp64"])
-@pytest.mark.parametrize("case", shoot_cases())
+@pytest.mark.parametrize("case", shoot_cases() + scheme_cases())
 def test_shoot_and_grad_match_reference(case, dtype):
     g = load_golden(case)
     tol = TOL[dtype]
@@ -305,12 +309,14 @@ def test_autograd_function_matches_engine():
     assert rel_l2(z0.grad[0].cpu() / 2.0, g["grad"]) < 1e-3
 
 
-def test_facade_directional_derivative_fp64_like_reference_suite():
-    """test_objective.py:117-129 restated through the device kernels (fp64)."""
+@pytest.mark.parametrize("scheme", ["semi-lagrangian", "eulerian", "hybrid"])
+def test_facade_directional_derivative_fp64_like_reference_suite(scheme):
+    """test_objective.py:117-129 / test_acceptance.py:75-90 (all schemes) restated
+    through the device kernels (fp64)."""
     import paper_2106_08817_b200 as mr
 
     g = load_golden("shoot_A_16sq.npz")
-    cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, 6, 0.05, mr.GaussianKernel(1.0), dtype=torch.float64)
+    cfg = mr.ShootingConfig(mr.Scheme(scheme), 6, 0.05, mr.GaussianKernel(1.0), dtype=torch.float64)
     geom = mr.GridGeometry(16, 16)
     prob = mr.RegistrationProblem(mr.ScalarField(geom, g["source"]), mr.ScalarField(geom, g["target"]),
                                   1e-3, 0.5, cfg)
@@ -390,3 +396,19 @@ def test_velocity_operators_match_oracle(B, H, W, R, split):
             gi = O.gradient(I[b])
             assert rel_l2(zb[b].cpu().numpy(), zb0[b] + (mbar * gi).sum(0)) < tol
             assert rel_l2(ib[b].cpu().numpy(), ib0[b] + O.gradient_adjoint(mbar * z[b])) < tol
+
+
+def test_schemes_are_2d_only_and_validated():
+    """Eulerian / Hybrid exist in 2D only (as in the reference); bad codes are FieldError."""
+    from paper_2106_08817_b200 import _lib
+    from paper_2106_08817_b200.errors import FieldError
+
+    eng = _eng()
+    traj = eng.allocate_trajectory(1, (8, 8, 8), 2, torch.float32)
+    with pytest.raises(FieldError):
+        eng.shoot_forward(traj, 0.1, np.array([0.25, 0.5, 0.25]), scheme="eulerian")
+    lib = _lib.load_library()
+    rc = lib.mr_shoot_forward_scheme(0, _lib.make_grid(1, (8, 8)),
+                                     _lib.KernelHandle(np.ones(3) / 3).struct, 7, 0.0, 2,
+                                     None, None, None, None, None, None, None)
+    assert rc == 1 and b"unknown scheme" in lib.mr_last_error()
