@@ -150,10 +150,12 @@ def run_ours(args):
     pairs = shard(B_global, rank, world)
     c = make_config(args.config, pairs=pairs)
     d = len(c.shape)
-    if d == 3 and c.mu > 0:  # untimed input preparation: keep shoots finite
+    if (d == 3 and c.mu > 0) or args.scheme != "semi-lagrangian":
+        # untimed input preparation: keep shoots finite (the explicit
+        # Eulerian continuity step is CFL-limited at the SL configs' 1 px/step)
         from paper_2106_08817_b200.calibrate import calibrate_no_divergence
 
-        calibrate_no_divergence(c)
+        calibrate_no_divergence(c, scheme=args.scheme)
     N = int(np.prod(c.shape))
     T = c.n_steps
     w = c.weights()

@@ -22,7 +22,8 @@ FACTORS = tuple(0.8 ** k for k in range(25))
 GROWTH = 10.0
 
 
-def calibrate_no_divergence(c, dtype=torch.float32, check_fp64: bool = True):
+def calibrate_no_divergence(c, dtype=torch.float32, check_fp64: bool = True,
+                            scheme: str = "semi-lagrangian"):
     """Scale ``c.z0`` in place, pair by pair, until no shoot diverges.
 
     Returns the per-pair scale factors (also stored in ``c.manifest``).
@@ -41,7 +42,7 @@ def calibrate_no_divergence(c, dtype=torch.float32, check_fp64: bool = True):
         while True:
             z = z_base * np.array([FACTORS[i] for i in idx]).reshape((-1,) + (1,) * len(c.shape))
             traj.z[0].copy_(torch.as_tensor(z, dtype=dt))
-            engine.shoot_forward(traj, c.mu, w)
+            engine.shoot_forward(traj, c.mu, w, scheme=scheme)
             bad = engine.diverged_pairs(traj.guard)
             zmax = traj.z.abs().flatten(2).amax(dim=2)  # [T+1, B]
             growth = (zmax.amax(dim=0) / zmax[0].clamp_min(1e-30)).cpu().numpy()

@@ -265,24 +265,6 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   const int gd0 = d_org + warp * kRB;
-  if (TRANSPOSE) {
-    if (gd0 <= 0 && gd0 + kRB > 0) {  // output row 0: sum_{d=0..R} W[R-d] g[d]
-      const int o = -gd0;
-      float2 a2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int dd = 0; dd <= R; ++dd) a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R - dd], a2);
-#pragma unroll
-      for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = a2;
-    }
-    if (gd0 <= D - 1 && gd0 + kRB > D - 1) {  // row n-1: sum_{d=-R..0} W[R+d] g[n-1+d]
-      const int o = D - 1 - gd0;
-      float2 a2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int dd = -R; dd <= 0; ++dd) a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R + dd], a2);
-#pragma unroll
-      for (int q = 0; q < kRB; ++q) if (q == o) acc[q] = a2;
-    }
-  }
   const long long gx = x0 + i;
   unsigned flags = 0;
   if (gx < HW) {
@@ -311,6 +293,36 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (EPI == 1 && guard && flags)
     atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / ncomp) * guard_stride), (int)flags);
+  if (TRANSPOSE && gx < HW) {
+    // edge rows 0 and n-1 of the transpose (cumulative-weight taps)
+    // overwrite what the interior formula stored there, after the accumulators
+    // are dead (keeps the main loop at the forward kernel's register count)
+    float* p = out + (long long)vol * D * HW + gx;
+    const bool pair = gx + 1 < HW && ((HW & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
+    auto put = [&](int gd, float2 val) {
+      float* r = p + (long long)gd * HW;
+      if (pair) {
+        *reinterpret_cast<float2*>(r) = val;
+      } else {
+        r[0] = val.x;
+        if (gx + 1 < HW) r[1] = val.y;
+      }
+    };
+    if (gd0 <= 0 && gd0 + kRB > 0) {  // output row 0: sum_{d=0..R} W[R-d] g[d]
+      const int o = -gd0;
+      float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int dd = 0; dd <= R; ++dd) a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R - dd], a2);
+      put(0, a2);
+    }
+    if (gd0 <= D - 1 && gd0 + kRB > D - 1) {  // row n-1: sum_{d=-R..0} W[R+d] g[n-1+d]
+      const int o = D - 1 - gd0;
+      float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int dd = -R; dd <= 0; ++dd) a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R + dd], a2);
+      put(D - 1, a2);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------
