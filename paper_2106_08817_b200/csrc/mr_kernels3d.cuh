@@ -192,13 +192,14 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 }
 
 // ------------------------------------------------------------------------------
-// fp32 axis-0 FIR (same contract as k_fir_axis0): tile of 64 columns x 64 outputs
+// fp32 axis-0 FIR (same contract as k_fir_axis0): tile of 64 columns x kA0D outputs
 // along D plus the R halo, staged with 16-B cp.async (row index clamped for the
 // forward, zero rows outside [0, D) for the transpose); one warp per block of
-// kRB output rows, lanes <-> column pairs, packed FFMA2.  FIR work is exactly
+// kA0RB output rows, lanes <-> column pairs, packed FFMA2.  FIR work is exactly
 // 2R+1 FFMA per output (the halo costs loads, not FLOPs).
 // ------------------------------------------------------------------------------
-constexpr int kA0X = 64, kA0D = 64;
+constexpr int kA0RB = 16;  // outputs per thread along axis 0 (register block)
+constexpr int kA0X = 64, kA0D = kNW * kA0RB;
 
 template <int R>
 struct Ax0F32Smem {
@@ -210,7 +211,7 @@ template <int R, bool TRANSPOSE, int EPI>
 __global__ void __launch_bounds__(kThreads)
     k_fir_axis0_f32(const float* __restrict__ in, float* out, int D, long long HW,
                     int32_t* guard, int guard_stride, int ncomp, Taps<float> tp) {
-  static_assert(kA0D == kNW * kRB && kA0X == 64, "one row block per warp, a column pair per lane");
+  static_assert(kA0D == kNW * kA0RB && kA0X == 64, "one row block per warp, a column pair per lane");
   extern __shared__ __align__(128) float rgf[];  // [RD][kA0X]
   constexpr int RD = Ax0F32Smem<R>::RD;
   const long long x0 = (long long)blockIdx.x * kA0X;
@@ -251,27 +252,27 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
 
   const int i = 2 * lane;
-  const float2* s2 = reinterpret_cast<const float2*>(rgf + warp * kRB * kA0X + i);
-  float2 acc[kRB];
+  const float2* s2 = reinterpret_cast<const float2*>(rgf + warp * kA0RB * kA0X + i);
+  float2 acc[kA0RB];
 #pragma unroll
-  for (int o = 0; o < kRB; ++o) acc[o] = make_float2(0.f, 0.f);
+  for (int o = 0; o < kA0RB; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int t = 0; t < kRB + 2 * R; ++t) {
+  for (int t = 0; t < kA0RB + 2 * R; ++t) {
     const float2 xv = s2[t * (kA0X / 2)];
 #pragma unroll
-    for (int o = 0; o < kRB; ++o) {
+    for (int o = 0; o < kA0RB; ++o) {
       const int tap = t - o;
       if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(xv, (float)tp.w[tap], acc[o]);
     }
   }
-  const int gd0 = d_org + warp * kRB;
+  const int gd0 = d_org + warp * kA0RB;
   const long long gx = x0 + i;
   unsigned flags = 0;
   if (gx < HW) {
     float* p = out + (long long)vol * D * HW + (long long)gd0 * HW + gx;
     const bool pair = gx + 1 < HW && ((HW & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
 #pragma unroll
-    for (int o = 0; o < kRB; ++o, p += HW) {
+    for (int o = 0; o < kA0RB; ++o, p += HW) {
       const int gd = gd0 + o;
       if (gd < D) {
         float2 val = acc[o];
@@ -308,14 +309,14 @@ __global__ void __launch_bounds__(kThreads)
         if (gx + 1 < HW) r[1] = val.y;
       }
     };
-    if (gd0 <= 0 && gd0 + kRB > 0) {  // output row 0: sum_{d=0..R} W[R-d] g[d]
+    if (gd0 <= 0 && gd0 + kA0RB > 0) {  // output row 0: sum_{d=0..R} W[R-d] g[d]
       const int o = -gd0;
       float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll 1
       for (int dd = 0; dd <= R; ++dd) a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R - dd], a2);
       put(0, a2);
     }
-    if (gd0 <= D - 1 && gd0 + kRB > D - 1) {  // row n-1: sum_{d=-R..0} W[R+d] g[n-1+d]
+    if (gd0 <= D - 1 && gd0 + kA0RB > D - 1) {  // row n-1: sum_{d=-R..0} W[R+d] g[n-1+d]
       const int o = D - 1 - gd0;
       float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll 1
