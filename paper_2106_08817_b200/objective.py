@@ -71,8 +71,8 @@ def cost(problem: RegistrationProblem, z0: ScalarField,
     return _report(terms[0].cpu().numpy())
 
 
-def grad(problem: RegistrationProblem, z0: ScalarField) -> ScalarField:
-    """Gradient of the discrete cost w.r.t. every entry of z0 (objective.py:91-174)."""
+def _shoot_device(problem: RegistrationProblem, z0: ScalarField) -> engine.DeviceTrajectory:
+    """The forward sweep of cost()/grad() on the device (raises IntegrationDiverged)."""
     if z0.geometry != problem.source.geometry:
         raise FieldError("initial momentum geometry mismatch")
     cfg = problem.cfg
@@ -81,6 +81,31 @@ def grad(problem: RegistrationProblem, z0: ScalarField) -> ScalarField:
     traj.z[0, 0].copy_(_to_device(z0, cfg.dtype))
     engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
     engine.raise_on_guard(traj)
+    return traj
+
+
+def _cost_and_trajectory(problem: RegistrationProblem, z0: ScalarField):
+    """cost() that also returns the device trajectory it shot, so a caller that
+    needs grad() at the same z0 can skip the forward."""
+    traj = _shoot_device(problem, z0)
+    J = _to_device(problem.target, traj.I.dtype).unsqueeze(0)
+    terms = engine.cost_terms(traj.I[0], traj.z[0], traj.v[0], traj.I[-1], J, problem.lam,
+                              problem.rho)
+    return _report(terms[0].cpu().numpy()), traj
+
+
+def grad(problem: RegistrationProblem, z0: ScalarField) -> ScalarField:
+    """Gradient of the discrete cost w.r.t. every entry of z0 (objective.py:91-174)."""
+    return _grad_on(problem, z0, _shoot_device(problem, z0))
+
+
+def _grad_on(problem: RegistrationProblem, z0: ScalarField,
+             traj: engine.DeviceTrajectory) -> ScalarField:
+    """grad() over an existing forward trajectory of z0 (the reverse sweep only).
+    The forward is deterministic, so this equals grad(problem, z0) exactly."""
+    if z0.geometry != problem.source.geometry:
+        raise FieldError("initial momentum geometry mismatch")
+    cfg = problem.cfg
     J = _to_device(problem.target, cfg.dtype).unsqueeze(0)
     bufs = engine.shoot_adjoint(traj, J, problem.lam, problem.rho, cfg.mu, cfg.kernel.weights,
                                 scheme=cfg.scheme.value)

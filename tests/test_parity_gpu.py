@@ -412,3 +412,51 @@ def test_schemes_are_2d_only_and_validated():
                                      _lib.KernelHandle(np.ones(3) / 3).struct, 7, 0.0, 2,
                                      None, None, None, None, None, None, None)
     assert rc == 1 and b"unknown scheme" in lib.mr_last_error()
+
+
+def test_optimize_reuses_trajectories_with_reference_iterates(monkeypatch):
+    """optimize() (optimizer.py:65-113) shoots once per cost evaluation only: the
+    gradient at an accepted point runs over that point's kept trajectory.  Its
+    iterates equal a plain loop over the public cost()/grad() (fp64)."""
+    import paper_2106_08817_b200 as mr
+    from paper_2106_08817_b200 import engine, optimizer
+
+    g = load_golden("shoot_E_40x33.npz")
+    cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, int(g["n_steps"]), float(g["mu"]),
+                            mr.GaussianKernel(float(g["sigma"]), int(g["radius"])),
+                            dtype=torch.float64)
+    geom = mr.GridGeometry(*g["source"].shape)
+    prob = mr.RegistrationProblem(mr.ScalarField(geom, g["source"]),
+                                  mr.ScalarField(geom, g["target"]), float(g["lam"]),
+                                  float(g["rho"]), cfg)
+    ocfg = mr.OptimizeConfig(max_iters=4)
+    calls = {"n": 0}
+    real = engine.shoot_forward
+
+    def counting(*a, **k):
+        calls["n"] += 1
+        return real(*a, **k)
+
+    monkeypatch.setattr(engine, "shoot_forward", counting)
+    res = optimizer.optimize(prob, mr.ScalarField(geom, g["z0"]), ocfg)
+    n_opt = calls["n"]
+    # the reference algorithm over the public API (one extra shoot per gradient)
+    z = mr.ScalarField(geom, g["z0"])
+    rep = mr.cost(prob, z)
+    totals, step = [rep.total], ocfg.init_step
+    for it in range(len(res.history) - 1):
+        gr = mr.grad(prob, z).values
+        gn = float(np.sum(gr * gr))
+        step = step / ocfg.backtrack_factor if it > 0 else ocfg.init_step
+        while True:
+            trial = mr.ScalarField(geom, z.values - step * gr)
+            tr = mr.cost(prob, trial)
+            if tr.total <= rep.total - ocfg.sufficient_decrease * step * gn:
+                break
+            step *= ocfg.backtrack_factor
+        z, rep = trial, tr
+        totals.append(rep.total)
+    assert [h.total for h in res.history] == pytest.approx(totals, rel=1e-12)
+    assert np.allclose(res.z0.values, z.values, rtol=1e-10, atol=1e-14)
+    n_evals = len(res.history) - 1
+    assert n_opt == calls["n"] - n_opt - n_evals  # the reference loop shot n_evals more times
