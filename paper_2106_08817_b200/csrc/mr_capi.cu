@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "mr_launch.cuh"
+#include "mr_kernels3d_k.cuh"
 #include "mr_tma.h"
 #include "mr_schemes2d.cuh"
 #include "mr_transport2d.cuh"
@@ -114,6 +115,18 @@ static dim3 grid3d(const Grid3& g) {
   return dim3((unsigned)((g.W + 31) / 32), (unsigned)((g.H + 7) / 8), (unsigned)(g.B * g.D));
 }
 
+// Multi-voxel 3D kernels: K voxels consecutive along axis 0 per thread.  Measured
+// on cfg4 (4 pairs, B200): product 60.5 / 42.8 / 38.9 us at K = 1 / 2 / 4; velocity-
+// adjoint epilogue 123 / 105 / 175 us.  The gather kernels (transport step,
+// divergence seed, transport adjoint) were slower at K > 1 (register-bound
+// occupancy: step 110 -> 124 us, adjoint 250 -> 343 us at K = 2) and stay at K = 1.
+constexpr int kProductK = 4, kEpiK = 2;
+
+static dim3 grid3d_k(const Grid3& g, int K) {
+  return dim3((unsigned)((g.W + 31) / 32), (unsigned)((g.H + 7) / 8),
+              (unsigned)(g.B * ((g.D + K - 1) / K)));
+}
+
 static unsigned flat_blocks(long long n) {
   long long b = (n + kThreads - 1) / kThreads;
   return (unsigned)(b < 148LL * 16 ? b : 148LL * 16);
@@ -126,7 +139,7 @@ static unsigned flat_blocks(long long n) {
 template <typename T>
 static int velocity3d(const Grid3& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
                       T* tmp, int32_t* guard, int guard_stride, cudaStream_t s) {
-  k_product3d<T><<<grid3d(g), kThreads, 0, s>>>(I, z, v, g);
+  k_product3d_k<T, kProductK><<<grid3d_k(g, kProductK), kThreads, 0, s>>>(I, z, v, g);
   int rc = cuda_status(cudaGetLastError());
   if (rc) return rc;
   Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};  // every (pair, component, slice) as a 2D image
@@ -404,7 +417,7 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
       e.flags = flags;
       k_veladj_epi3d<T, true><<<grid3d(g), kThreads, 0, s>>>(e);
     } else {
-      k_veladj_epi3d<T, false><<<grid3d(g), kThreads, 0, s>>>(e);
+      k_veladj_epi3d_k<T, kEpiK><<<grid3d_k(g, kEpiK), kThreads, 0, s>>>(e);
     }
     if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "veladj_epi3d");
     T* t = cur;
