@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads)
 template <typename T>
 struct Plan3 {
   AxisPlan<T> a[3];
-  long long base;
+  long long base;  // 64-bit: measured faster than int here (IMAD.WIDE addressing)
 };
 
 template <typename T>
@@ -561,18 +561,43 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   const T* __restrict__ s = a.s + b * g.N;
   const T a0 = v0[q], a1 = v1[q], a2 = v2[q];
   const T ib_ = a.ibar[b * g.N + q], zb_ = a.zbar[b * g.N + q];
-  const T vm0 = d > 0 ? v0[q - g.HW] : a0, vp0 = d < g.D - 1 ? v0[q + g.HW] : a0;
-  const T vm1 = y > 0 ? v1[q - g.W] : a1, vp1 = y < g.H - 1 ? v1[q + g.W] : a1;
-  const T vm2 = x > 0 ? v2[q - 1] : a2, vp2 = x < g.W - 1 ? v2[q + 1] : a2;
   const int st[3] = {(int)g.HW, g.W, 1};
   const int pos[3] = {d, y, x};
   const int n[3] = {g.D, g.H, g.W};
+  // Interior voxels (2 <= pos <= n-3 on every axis): the np.gradient stencil and
+  // the gather form of its transpose have no edge terms, so neighbour loads are
+  // unconditional and D^T s is 0.5 s[j-1] - 0.5 s[j+1] -- the same operations
+  // diff_adj1 performs there (bitwise equal).  Only the loads and the stencil
+  // arithmetic branch; the scatters below stay warp-converged.
+  const bool inner = own && d >= 2 && d <= g.D - 3 && y >= 2 && y <= g.H - 3 && x >= 2 &&
+                     x <= g.W - 3;
+  T vm0, vp0, vm1, vp1, vm2, vp2;
   T sm[3], sp[3];
   const T sc = s[q];
+  if (inner) {
+    vm0 = v0[q - g.HW];
+    vp0 = v0[q + g.HW];
+    vm1 = v1[q - g.W];
+    vp1 = v1[q + g.W];
+    vm2 = v2[q - 1];
+    vp2 = v2[q + 1];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    sm[c] = pos[c] > 0 ? s[q - st[c]] : T(0);
-    sp[c] = pos[c] < n[c] - 1 ? s[q + st[c]] : T(0);
+    for (int c = 0; c < 3; ++c) {
+      sm[c] = s[q - st[c]];
+      sp[c] = s[q + st[c]];
+    }
+  } else {
+    vm0 = d > 0 ? v0[q - g.HW] : a0;
+    vp0 = d < g.D - 1 ? v0[q + g.HW] : a0;
+    vm1 = y > 0 ? v1[q - g.W] : a1;
+    vp1 = y < g.H - 1 ? v1[q + g.W] : a1;
+    vm2 = x > 0 ? v2[q - 1] : a2;
+    vp2 = x < g.W - 1 ? v2[q + 1] : a2;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sm[c] = pos[c] > 0 ? s[q - st[c]] : T(0);
+      sp[c] = pos[c] < n[c] - 1 ? s[q + st[c]] : T(0);
+    }
   }
   const Plan3<T> p = plan3<T>(d, y, x, a0, a1, a2, a.dt, g);
   const int base = (int)p.base;
@@ -583,8 +608,9 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   T w8[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) w8[c] = axis_w(p, c, 0) * axis_w(p, c, 1) * axis_w(p, c, 2);
-  const T div = grad1(vm0, a0, vp0, d, g.D) + grad1(vm1, a1, vp1, y, g.H) +
-                grad1(vm2, a2, vp2, x, g.W);
+  const T div = inner ? (vp0 - vm0) / T(2) + (vp1 - vm1) / T(2) + (vp2 - vm2) / T(2)
+                     : grad1(vm0, a0, vp0, d, g.D) + grad1(vm1, a1, vp1, y, g.H) +
+                           grad1(vm2, a2, vp2, x, g.W);
   const T wz = zb_ * (T(1) - a.dt * div);
   T dI[3], dz[3];
   coord_grad3(cI, p, dI);
@@ -594,12 +620,17 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   for (int c = 0; c < 3; ++c) vb[c] = -a.dt * dI[c] * ib_;
 #pragma unroll
   for (int c = 0; c < 3; ++c) vb[c] += -a.dt * dz[c] * wz;
+  if (inner) {
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {  // vbar_c += D_c^T s (gather form along each axis)
-    const int j = pos[c];
-    const T sf = j == 0 ? sc : (j == 1 ? sm[c] : T(0));
-    const T sl = j == n[c] - 1 ? sc : (j == n[c] - 2 ? sp[c] : T(0));
-    vb[c] += diff_adj1(sm[c], sp[c], sf, sl, j, n[c]);
+    for (int c = 0; c < 3; ++c) vb[c] += T(0.5) * sm[c] - T(0.5) * sp[c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // vbar_c += D_c^T s (gather form along each axis)
+      const int j = pos[c];
+      const T sf = j == 0 ? sc : (j == 1 ? sm[c] : T(0));
+      const T sl = j == n[c] - 1 ? sc : (j == n[c] - 2 ? sp[c] : T(0));
+      vb[c] += diff_adj1(sm[c], sp[c], sf, sl, j, n[c]);
+    }
   }
 
   T* __restrict__ ibo = a.ib + b * g.N;

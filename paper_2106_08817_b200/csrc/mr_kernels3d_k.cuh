@@ -87,26 +87,43 @@ __global__ void __launch_bounds__(kThreads) k_veladj_epi3d_k(VelAdj3Args<T> a) {
   }
   T iu[K], id[K], il[K], ir[K], m1[K], m2[K], zb[K], ib[K];
   T k1m[K], k1p[K], z1m[K], z1p[K], k2m[K], k2p[K], z2m[K], z2p[K];
+  // in-plane interior (2 <= y <= H-3, 2 <= x <= W-3): no edge terms on axes 1, 2
+  const bool inner_yx = y >= 2 && y <= g.H - 3 && x >= 2 && x <= g.W - 3;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int q = q0 + (min(d0 + j, g.D - 1) - d0) * HW;
     const T c = ci[j + 1];
-    iu[j] = y > 0 ? I[q - g.W] : c;
-    id[j] = y < g.H - 1 ? I[q + g.W] : c;
-    il[j] = x > 0 ? I[q - 1] : c;
-    ir[j] = x < g.W - 1 ? I[q + 1] : c;
     m1[j] = k1[q];
     m2[j] = k2[q];
     zb[j] = a.zb[pb + q];
     ib[j] = a.ib[pb + q];
-    k1m[j] = y > 0 ? k1[q - g.W] : T(0);
-    z1m[j] = y > 0 ? z[q - g.W] : T(0);
-    k1p[j] = y < g.H - 1 ? k1[q + g.W] : T(0);
-    z1p[j] = y < g.H - 1 ? z[q + g.W] : T(0);
-    k2m[j] = x > 0 ? k2[q - 1] : T(0);
-    z2m[j] = x > 0 ? z[q - 1] : T(0);
-    k2p[j] = x < g.W - 1 ? k2[q + 1] : T(0);
-    z2p[j] = x < g.W - 1 ? z[q + 1] : T(0);
+    if (inner_yx) {
+      iu[j] = I[q - g.W];
+      id[j] = I[q + g.W];
+      il[j] = I[q - 1];
+      ir[j] = I[q + 1];
+      k1m[j] = k1[q - g.W];
+      z1m[j] = z[q - g.W];
+      k1p[j] = k1[q + g.W];
+      z1p[j] = z[q + g.W];
+      k2m[j] = k2[q - 1];
+      z2m[j] = z[q - 1];
+      k2p[j] = k2[q + 1];
+      z2p[j] = z[q + 1];
+    } else {
+      iu[j] = y > 0 ? I[q - g.W] : c;
+      id[j] = y < g.H - 1 ? I[q + g.W] : c;
+      il[j] = x > 0 ? I[q - 1] : c;
+      ir[j] = x < g.W - 1 ? I[q + 1] : c;
+      k1m[j] = y > 0 ? k1[q - g.W] : T(0);
+      z1m[j] = y > 0 ? z[q - g.W] : T(0);
+      k1p[j] = y < g.H - 1 ? k1[q + g.W] : T(0);
+      z1p[j] = y < g.H - 1 ? z[q + g.W] : T(0);
+      k2m[j] = x > 0 ? k2[q - 1] : T(0);
+      z2m[j] = x > 0 ? z[q - 1] : T(0);
+      k2p[j] = x < g.W - 1 ? k2[q + 1] : T(0);
+      z2p[j] = x < g.W - 1 ? z[q + 1] : T(0);
+    }
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -129,13 +146,21 @@ __global__ void __launch_bounds__(kThreads) k_veladj_epi3d_k(VelAdj3Args<T> a) {
     const int pos[3] = {d, y, x};
     const int n[3] = {g.D, g.H, g.W};
     T acc = T(0);
+    if (inner_yx && d >= 2 && d <= g.D - 3) {  // diff_adj1 without edge terms
 #pragma unroll
-    for (int cc = 0; cc < 3; ++cc) {
-      const int jj = pos[cc];
-      const T gf = jj == 0 ? qcv[cc] : (jj == 1 ? qmv[cc] : T(0));
-      const T gl = jj == n[cc] - 1 ? qcv[cc] : (jj == n[cc] - 2 ? qpv[cc] : T(0));
-      const T t = diff_adj1(qmv[cc], qpv[cc], gf, gl, jj, n[cc]);
-      acc = (cc == 0) ? t : acc + t;
+      for (int cc = 0; cc < 3; ++cc) {
+        const T t = T(0.5) * qmv[cc] - T(0.5) * qpv[cc];
+        acc = (cc == 0) ? t : acc + t;
+      }
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const int jj = pos[cc];
+        const T gf = jj == 0 ? qcv[cc] : (jj == 1 ? qmv[cc] : T(0));
+        const T gl = jj == n[cc] - 1 ? qcv[cc] : (jj == n[cc] - 2 ? qpv[cc] : T(0));
+        const T t = diff_adj1(qmv[cc], qpv[cc], gf, gl, jj, n[cc]);
+        acc = (cc == 0) ? t : acc + t;
+      }
     }
     a.ib[pp] = ib[j] + acc;
   }
