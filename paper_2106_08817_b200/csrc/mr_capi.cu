@@ -245,7 +245,8 @@ static int launch_cost_terms2d(const Grid2& g, double lam, double rho, const T* 
   cudaError_t e = cudaMemsetAsync(terms, 0, sizeof(double) * 4 * g.B, s);
   if (e != cudaSuccess) return MR_ECUDA;
   CostArgs<T> a{I0, z0, v0, IT, J, seed, terms, g};
-  long long blocks = (g.N + kThreads * 4 - 1) / (kThreads * 4);
+  // one warp per row: blocks of kNW rows
+  long long blocks = (g.H + kNW - 1) / kNW;
   if (blocks > 1024) blocks = 1024;
   k_cost_terms2d<T><<<dim3((unsigned)blocks, g.B), kThreads, 0, s>>>(a);
   k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, g.B, lam, rho);

@@ -1486,17 +1486,20 @@ __global__ void __launch_bounds__(kThreads) k_cost_terms2d(CostArgs<T> a) {
   const T* __restrict__ IT = a.IT + b * N;
   const T* __restrict__ J = a.J + b * N;
   double data = 0.0, vn = 0.0, zn = 0.0;
-  for (long long q = blockIdx.x * (long long)kThreads + threadIdx.x; q < N;
-       q += (long long)gridDim.x * kThreads) {
-    T diff = IT[q] - J[q];
-    if (a.seed) a.seed[b * N + q] = diff;
-    data += (double)diff * (double)diff;
-    int y = (int)(q / W), x = (int)(q - (long long)y * W);
-    T g0, g1;
-    grad2(I0, y, x, H, W, g0, g1);
-    T zz = z0[q];
-    vn += (double)(zz * g0) * (double)w0[q] + (double)(zz * g1) * (double)w0[N + q];
-    zn += (double)zz * (double)zz;
+  // warp <-> row, lanes <-> consecutive columns (no per-element index division)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int y = blockIdx.x * kNW + warp; y < H; y += gridDim.x * kNW) {
+    for (int x = lane; x < W; x += 32) {
+      const long long q = (long long)y * W + x;
+      T diff = IT[q] - J[q];
+      if (a.seed) a.seed[b * N + q] = diff;
+      data += (double)diff * (double)diff;
+      T g0, g1;
+      grad2(I0, y, x, H, W, g0, g1);
+      T zz = z0[q];
+      vn += (double)(zz * g0) * (double)w0[q] + (double)(zz * g1) * (double)w0[N + q];
+      zn += (double)zz * (double)zz;
+    }
   }
   double s;
   s = block_sum(data, red);
