@@ -59,7 +59,36 @@ def parse():
     p.add_argument("--e2e-chunks", type=int, default=None,
                    help="pair groups of the host-buffer pipeline (default: the API's choice)")
     p.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
+    p.add_argument("--print-launch", action="store_true",
+                   help="print the multi-rank launch command --gpus N would exec, then exit")
     return p.parse_args()
+
+
+def launch_cmd(argv, n: int, port: int) -> list:
+    """torch.distributed.run command that starts one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def maybe_relaunch(args) -> bool:
+    """`python bench.py --gpus N` outside torchrun: re-exec as N ranks (one per GPU).
+    Returns True when this process only launched (and waited for) the ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as sk:  # a free local port for the rendezvous
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = launch_cmd(sys.argv[1:], args.gpus, port)
+    if args.print_launch:
+        print(json.dumps({"launch": cmd}))
+        return True
+    rc = subprocess.call(cmd)
+    if rc != 0:
+        sys.exit(rc)
+    return True
 
 
 def dist_env():
@@ -144,6 +173,12 @@ def run_ours(args):
     from paper_2106_08817_b200.synthetic import CONFIGS, make_config
 
     rank, world, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"bench: {world} rank(s) from the launcher, --gpus {args.gpus}; using {world}",
+              file=sys.stderr)
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench: rank {rank} needs GPU {local}, only "
+                         f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -456,7 +491,9 @@ def run_reference(args):
         return
     cores = len(os.sched_getaffinity(0))
     spec = CONFIGS[args.config]
-    T_sample = min(spec["n_steps"], 5 if len(spec["shape"]) == 2 else 1)
+    # 2D: the full T of the config (same_config); 3D: one step (cost per voxel-step is
+    # T-independent and a full-T 3D oracle grad takes minutes per pair)
+    T_sample = spec["n_steps"] if len(spec["shape"]) == 2 else 1
     P = min(cores, spec["batch"])
     c = make_config(args.config, batch=P)
     w = c.weights()
@@ -487,9 +524,10 @@ def run_reference(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded cfg-2 generator, same as the GPU arm)",
-        "config": {"workload": f"{c.name}: {P} of {spec['batch']} pairs per step, T={T_sample} "
-                               f"(truncated from {spec['n_steps']}; cost is linear in T)",
+        "data": f"synthetic (seeded cfg-{args.config} generator, same as the GPU arm)",
+        "config": {"workload": f"{c.name}: {P} of {spec['batch']} pairs per step, T={T_sample}"
+                               + ("" if T_sample == spec["n_steps"] else
+                                  f" (truncated from {spec['n_steps']}; cost is linear in T)"),
                    "global_batch": spec["batch"], "shape": list(c.shape)},
         "cpu_baseline": {"value": value, "unit": "voxel-steps/s", "cores": cores, "kind": "port",
                          "sample": f"{P} pairs x T={T_sample} per step, one pair per process, "
@@ -503,6 +541,8 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    if maybe_relaunch(a):
+        sys.exit(0)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -121,6 +121,65 @@ int mr_velocity_adjoint(int dtype, mr_grid g, mr_kernel k, const void* I,
                         const void* z, const void* vbar, void* ib, void* zb,
                         void* workspace, void* stream);
 
+/* One transport step of any Scheme with an explicit dt -- the field-level
+ * single-step operations advect_image_sl / continuity_sl (scheme SL,
+ * integrator.py:141-159) and advect_image_euler / continuity_euler (EULERIAN,
+ * integrator.py:133-138, 154-155).  I' and z' are both written; callers of a
+ * one-output reference function discard the other.  Eulerian / Hybrid are 2D. */
+int mr_scheme_step(int dtype, mr_grid g, int32_t scheme, double dt, double mu,
+                   const void* I, const void* z, const void* v, void* I_next,
+                   void* z_next, const void* phi_in, void* phi_out, void* stream);
+
+/* ---- array-level operators (fields.py:144-262, kernel.py:36-68) ----------- *
+ * Not on the shooting hot path (the whole-loop kernels fuse them); exported so
+ * the facade is a drop-in for code that calls the operators one by one.
+ * 2D or 3D grids; scalar batch [B][N], vector batch [B][d][N]. */
+
+/* axis_diff (np.gradient, fields.py:144-145) along `axis`, or its exact
+ * transpose axis_diff_adjoint (fields.py:148-158) when adjoint != 0. */
+int mr_axis_diff(int dtype, mr_grid g, int32_t axis, const void* a, void* out,
+                 int32_t adjoint, void* stream);
+
+/* gradient_arr (fields.py:161-162): f [B][N] -> out [B][d][N]; with
+ * adjoint != 0 its transpose gradient_adjoint_arr (fields.py:165-166):
+ * f = gbar [B][d][N] -> out [B][N]. */
+int mr_gradient(int dtype, mr_grid g, const void* f, void* out, int32_t adjoint,
+                void* stream);
+
+/* divergence_arr (fields.py:169-170): v [B][d][N] -> out [B][N]. */
+int mr_divergence(int dtype, mr_grid g, const void* v, void* out, void* stream);
+
+/* conv1d_replicate (kernel.py:36-45) along `axis`, or its exact transpose
+ * conv1d_replicate_adjoint (kernel.py:48-68) when adjoint != 0. */
+int mr_conv1d(int dtype, mr_grid g, mr_kernel k, int32_t axis, const void* a,
+              void* out, int32_t adjoint, void* stream);
+
+/* bilinear_plan + bilinear_apply (fields.py:207-240; trilinear in 3D) of
+ * ncomp components a [B][ncomp][N] at absolute sample coordinates
+ * coords [B][d][N] (channel c = coordinate along axis c) -> out [B][ncomp][N].
+ * bad: nullable int32 device flag, set to 1 when a coordinate is non-finite
+ * (bilinear_plan raises FieldError, fields.py:208-209). */
+int mr_interpolate(int dtype, mr_grid g, const void* coords, const void* a,
+                   void* out, int32_t ncomp, int32_t* bad, void* stream);
+
+/* bilinear_adjoint_values (fields.py:243-254): out [B][N] = B^T gbar
+ * (zero-filled by the library, then scattered). */
+int mr_interpolate_adjoint(int dtype, mr_grid g, const void* coords,
+                           const void* gbar, void* out, int32_t* bad,
+                           void* stream);
+
+/* bilinear_coord_grad (fields.py:257-262): out [B][d][N], derivative of the
+ * interpolated value w.r.t. each coordinate times the strict inside mask. */
+int mr_interpolate_coord_grad(int dtype, mr_grid g, const void* coords,
+                              const void* a, void* out, int32_t* bad,
+                              void* stream);
+
+/* Per-pair reductions, fp64 accumulation, deterministic order: op 0 = dot
+ * (fields.py:285-288) sum a*b; op 1 = ssd (fields.py:291-295) 0.5 sum (a-b)^2;
+ * op 2 = sum a^2 (b unused).  out: double[B] device. */
+int mr_reduce(int dtype, mr_grid g, int32_t op, const void* a, const void* b,
+              double* out, void* stream);
+
 /* ---- whole-loop entry points (one call per shoot / gradient) -------------- */
 
 /* Bytes of device workspace mr_shoot_forward uses: 3 scalars per voxel in 3D,

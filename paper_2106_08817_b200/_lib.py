@@ -48,6 +48,15 @@ EXPORTS = (
     "mr_shoot_adjoint_scheme",
     "mr_cost_terms",
     "mr_smooth",
+    "mr_scheme_step",
+    "mr_axis_diff",
+    "mr_gradient",
+    "mr_divergence",
+    "mr_conv1d",
+    "mr_interpolate",
+    "mr_interpolate_adjoint",
+    "mr_interpolate_coord_grad",
+    "mr_reduce",
     "mr_last_error",
     "mr_strerror",
     "mr_version",
@@ -87,6 +96,15 @@ _SIGNATURES = {
     ),
     "mr_cost_terms": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_smooth": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _i32, _vp]),
+    "mr_scheme_step": (_i32, [_i32, MrGrid, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_axis_diff": (_i32, [_i32, MrGrid, _i32, _vp, _vp, _i32, _vp]),
+    "mr_gradient": (_i32, [_i32, MrGrid, _vp, _vp, _i32, _vp]),
+    "mr_divergence": (_i32, [_i32, MrGrid, _vp, _vp, _vp]),
+    "mr_conv1d": (_i32, [_i32, MrGrid, MrKernel, _i32, _vp, _vp, _i32, _vp]),
+    "mr_interpolate": (_i32, [_i32, MrGrid, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "mr_interpolate_adjoint": (_i32, [_i32, MrGrid, _vp, _vp, _vp, _vp, _vp]),
+    "mr_interpolate_coord_grad": (_i32, [_i32, MrGrid, _vp, _vp, _vp, _vp, _vp]),
+    "mr_reduce": (_i32, [_i32, MrGrid, _i32, _vp, _vp, _vp, _vp]),
     "mr_last_error": (ctypes.c_char_p, []),
     "mr_strerror": (ctypes.c_char_p, [_i32]),
     "mr_version": (_i32, []),

@@ -27,6 +27,8 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+
 static int check_cuda(const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MR_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -174,8 +176,7 @@ static int launch_sl_step2d(const Grid2& g, double dt, double mu, const T* I, co
     if (make_map3<T>(&m.I, I, g.W, g.H, g.B, C::GX, C::GY) &&
         make_map3<T>(&m.z, z, g.W, g.H, g.B, C::GX, C::GY) &&
         make_map3<T>(&m.v, v, g.W, g.H, 2LL * g.B, C::VX, C::VY)) {
-      static const cudaError_t attr = cudaFuncSetAttribute(
-          k_sl_step2d_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
+      const cudaError_t attr = ensure_smem<k_sl_step2d_tma<T>>(C::bytes);
       if (attr != cudaSuccess) return cuda_status(attr);
       dim3 grid((g.W + C::TX - 1) / C::TX, (g.H + C::TY - 1) / C::TY, g.B);
       k_sl_step2d_tma<T><<<grid, kThreads, C::bytes, s>>>(a, m);
@@ -201,8 +202,7 @@ static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I,
         make_map3<T>(&m.ibar, ibar, g.W, g.H, g.B, C::VX, C::VY) &&
         make_map3<T>(&m.zbar, zbar, g.W, g.H, g.B, C::VX, C::VY)) {
       constexpr size_t bytes = AdjCfg<T>::bytes;
-      static const cudaError_t attr = cudaFuncSetAttribute(
-          k_sl_adjoint2d_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      const cudaError_t attr = ensure_smem<k_sl_adjoint2d_tma<T>>(bytes);
       if (attr != cudaSuccess) return cuda_status(attr);
       dim3 grid((g.W + C::TX - 1) / C::TX, (g.H + C::TY - 1) / C::TY, g.B);
       k_sl_adjoint2d_tma<T><<<grid, kThreads, bytes, s>>>(a, m);
@@ -594,6 +594,32 @@ int mr_sl_step(int dtype, mr_grid g, double dt, double mu, const void* I, const 
                                             (const double*)phi_in, (double*)phi_out,
                                             as_stream(stream)));
   return check_rc(rc, "mr_sl_step");
+}
+
+int mr_scheme_step(int dtype, mr_grid g, int32_t scheme, double dt, double mu, const void* I,
+                   const void* z, const void* v, void* I_next, void* z_next, const void* phi_in,
+                   void* phi_out, void* stream) {
+  if (scheme == MR_SCHEME_SEMI_LAGRANGIAN)
+    return mr_sl_step(dtype, g, dt, mu, I, z, v, I_next, z_next, phi_in, phi_out, stream);
+  if (scheme != MR_SCHEME_EULERIAN && scheme != MR_SCHEME_HYBRID)
+    return fail(MR_EINVAL, "unknown scheme");
+  int rc = validate(dtype, g, false);
+  if (rc) return rc;
+  if (!I || !z || !v || !I_next || !z_next) return fail(MR_EINVAL, "NULL field pointer");
+  if ((phi_in == nullptr) != (phi_out == nullptr))
+    return fail(MR_EINVAL, "phi_in and phi_out must both be set or both be NULL");
+  Grid2 g2 = grid2(g);
+  rc = MR_DISPATCH(dtype,
+                   launch_scheme_step2d<float>(scheme, g2, dt, mu, (const float*)I, (const float*)z,
+                                               (const float*)v, (float*)I_next, (float*)z_next,
+                                               (const float*)phi_in, (float*)phi_out,
+                                               as_stream(stream), nullptr, nullptr, 1),
+                   launch_scheme_step2d<double>(scheme, g2, dt, mu, (const double*)I,
+                                                (const double*)z, (const double*)v,
+                                                (double*)I_next, (double*)z_next,
+                                                (const double*)phi_in, (double*)phi_out,
+                                                as_stream(stream), nullptr, nullptr, 1));
+  return check_rc(rc, "mr_scheme_step");
 }
 
 int mr_sl_step_adjoint(int dtype, mr_grid g, double dt, double mu, const void* I, const void* z,

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/morphreg_sm100.h"
 
 namespace mr {
@@ -31,6 +33,23 @@ struct Grid2 {
   int B, H, W;
   long long N;  // H*W
 };
+
+// One-time cudaFuncSetAttribute(MaxDynamicSharedMemorySize) per (kernel, device):
+// the attribute is per device, so a process that drives several GPUs sets it on
+// each; a failed call is not cached (the next launch retries).
+constexpr int kMaxDevices = 64;
+template <auto Kernel>
+inline cudaError_t ensure_smem(size_t bytes) {
+  static std::atomic<int> done[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const bool cached = dev >= 0 && dev < kMaxDevices;
+  if (cached && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && cached) done[dev].store(1, std::memory_order_release);
+  return e;
+}
 
 // ---- finite differences (fields.py:144-158) ------------------------------------
 

@@ -1,2 +1,5 @@
-#include "mr_fir_impl.cuh"
+#include "mr_fir_axis0.cuh"
+namespace mr {
+MR_RADIUS_LIST(MR_AX0_EXTERN_F32)
+}
 MR_INSTANTIATE_AXIS0(float)

@@ -1,0 +1,4 @@
+#include "mr_fir_axis0.cuh"
+namespace mr {
+MR_AX0_GROUP0(MR_AX0_INST_F64)
+}

@@ -2,7 +2,6 @@
 #pragma once
 
 #include "mr_launch.cuh"
-#include "mr_stream2d.cuh"
 #include "mr_tma.h"
 
 namespace mr {
@@ -11,35 +10,6 @@ inline dim3 fir_grid(int W, int H, int B, int tx, int ty) {
   return dim3((unsigned)((W + tx - 1) / tx), (unsigned)((H + ty - 1) / ty), (unsigned)B);
 }
 
-// Column-strip streaming kernel (fp32, TMA-describable layouts); returns 1 when
-// not applicable so the caller falls back to the tile kernel.
-template <typename T, int R>
-int velocity_stream_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) {
-  if constexpr (sizeof(T) != 4) {
-    return 1;  // fp64 (parity path) keeps the tile kernel
-  } else {
-  using C = StreamCfg<T, R>;
-  if (C::bytes > 227 * 1024) return 1;
-  // one CTA per strip walks all rows: only worth it with ~1 strip per SM or more
-  // (the host pipeline runs 4 groups of pairs concurrently, 128 strips each at cfg2)
-  if ((long long)((g.W + C::OX - 1) / C::OX) * g.B < 128) return 1;
-  CUtensorMap mI, mZ;
-  if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, C::PXI, C::G + 2) ||
-      !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, C::PXZ, C::G))
-    return 1;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      k_velocity2d_stream<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes);
-  if (attr != cudaSuccess) return cuda_status(attr);
-  a.use_tma = 1;
-  dim3 grid((unsigned)((g.W + C::OX - 1) / C::OX), (unsigned)g.B);
-  k_velocity2d_stream<T, R><<<grid, kThreads, C::bytes, s>>>(a, tp, mI, mZ);
-  return cuda_status(cudaGetLastError());
-  }
-}
-
-template <typename T, int R, bool TR, int EPI>
-int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s);
 
 // Split velocity (fp32, scratch given): product +
 // axis-1 FIR per tile (k_velocity2d_h) into a.vtmp, then the axis-0 FIR over whole
@@ -56,15 +26,14 @@ int velocity_split_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream
     if (!make_map3<T>(&mI, a.I, g.W, g.H, g.B, V::PXI, S::OY + 2) ||
         !make_map3<T>(&mZ, a.z, g.W, g.H, g.B, V::PXZ, S::OY))
       return 1;
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        k_velocity2d_h<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V::bytes);
+    const cudaError_t attr = ensure_smem<k_velocity2d_h<R>>(V::bytes);
     if (attr != cudaSuccess) return cuda_status(attr);
     k_velocity2d_h<R><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, V::bytes, s>>>(
         a, tp, mI, mZ, a.vtmp);
     int rc = cuda_status(cudaGetLastError());
     if (rc) return rc;
-    return fir_axis0_r<T, R, false, 1>(tp, a.vtmp, a.v, 2 * g.B, g.H, (long long)g.W, a.guard,
-                                       a.guard_stride, 2, s);
+    return launch_fir_axis0<T>(R, tp, a.vtmp, a.v, 2 * g.B, g.H, (long long)g.W, false, 1,
+                               a.guard, a.guard_stride, 2, s);
   }
 }
 
@@ -74,15 +43,10 @@ int velocity_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream_t s) 
     int rc = velocity_split_r<T, R>(g, tp, a, s);
     if (rc != 1) return rc;
   }
-  {
-    int rc = velocity_stream_r<T, R>(g, tp, a, s);
-    if (rc != 1) return rc;
-  }
   using S = FirSmem<T, R, 2>;
   using V = VelSmem<T, R>;
   constexpr size_t bytes = V::bytes;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      k_velocity2d<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const cudaError_t attr = ensure_smem<k_velocity2d<T, R>>(bytes);
   if (attr != cudaSuccess) return cuda_status(attr);
   CUtensorMap mI, mZ;
   a.use_tma = make_map3<T>(&mI, a.I, g.W, g.H, g.B, V::PXI, S::RY + 2) &&
@@ -99,57 +63,18 @@ int smooth_r(const Grid2& g, const Taps<T>& tp, const SmoothArgs<T>& a, cudaStre
     CUtensorMap m;
     if (g.N < (1LL << 31) && make_map3<T>(&m, a.a, g.W, g.H, g.B, S::PX, S::RY)) {
       constexpr size_t bytes = SmoothTmaSmem<R>::bytes;
-      static const cudaError_t attr = cudaFuncSetAttribute(
-          k_smooth2d_tma<R, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      const cudaError_t attr = ensure_smem<k_smooth2d_tma<R, TR>>(bytes);
       if (attr != cudaSuccess) return cuda_status(attr);
       k_smooth2d_tma<R, TR><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, bytes, s>>>(a, tp, m);
       return cuda_status(cudaGetLastError());
     }
   }
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      k_smooth2d<T, R, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  const cudaError_t attr = ensure_smem<k_smooth2d<T, R, TR>>(S::bytes);
   if (attr != cudaSuccess) return cuda_status(attr);
   k_smooth2d<T, R, TR><<<fir_grid(g.W, g.H, g.B, S::OX, S::OY), kThreads, S::bytes, s>>>(a, tp);
   return cuda_status(cudaGetLastError());
 }
 
-template <typename T, int R, bool REG>
-int veladj_stream_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s) {
-  // FIR work 2*(2R+1) FFMA per computed output (no y halo), 62/64 x 30/32 owners.
-  // Measured on B200 (cfg2, FFMA2 passes, interior epilogue): 0.331 ms against
-  // 0.294 ms for the tile kernel (exposed vbar TMA at each block start: the
-  // staging buffer doubles as the epilogue's I/z tile).  Kept for tuning.
-  constexpr bool kEnabled = false;
-  if constexpr (sizeof(T) != 4 || !kEnabled) {
-    return 1;
-  } else {
-    using C = StreamAdjCfg<T, R>;
-    constexpr size_t bytes = REG ? C::bytes_reg : C::bytes_noreg;
-    if (bytes > 227 * 1024) return 1;
-    if ((long long)((g.W + C::OX - 3) / (C::OX - 2)) * g.B < 128) return 1;
-    VelAdjMaps m;
-    const long long B2 = 2LL * g.B;
-    const bool ok = make_map3<T>(&m.vbar, a.vbar, g.W, g.H, B2, C::PXZ, C::G) &&
-                    make_map3<T>(&m.I, a.I, g.W, g.H, g.B, C::OXP, C::G) &&
-                    make_map3<T>(&m.z, a.z, g.W, g.H, g.B, C::OXP, C::G) &&
-                    (REG ? make_map3<T>(&m.op2, a.v0, g.W, g.H, B2, C::OXP, C::G)
-                         : make_map3<T>(&m.op2, a.ib, g.W, g.H, g.B, C::OXP, C::G)) &&
-                    make_map3<T>(&m.zb, a.zb, g.W, g.H, g.B, C::OXP, C::G);
-    if (!ok) return 1;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(k_velocity_adj2d_stream<T, R, REG>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (attr != cudaSuccess) return cuda_status(attr);
-    a.use_tma = 1;
-    dim3 grid((unsigned)((g.W + C::OX - 3) / (C::OX - 2)), (unsigned)g.B);
-    k_velocity_adj2d_stream<T, R, REG><<<grid, kAdjStreamThreads, bytes, s>>>(a, tp, m);
-    return cuda_status(cudaGetLastError());
-  }
-}
-
-template <typename T, int R, bool TR, int EPI>
-int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s);
 
 // Split velocity adjoint (fp32, scratch given): whole-column axis-0 transposed FIR
 // into a.vtmp (k_fir_axis0_f32), then the axis-1 pass + epilogue
@@ -169,12 +94,11 @@ int veladj_split_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStrea
                     make_map3<T>(&m.I, a.I, g.W, g.H, g.B, V::OXP, S::OY) &&
                     make_map3<T>(&m.z, a.z, g.W, g.H, g.B, V::OXP, S::OY);
     if (!ok) return 1;
-    int rc = fir_axis0_r<T, R, true, 0>(tp, a.vbar, a.vtmp, (int)B2, g.H, (long long)g.W, nullptr,
-                                        0, 2, s);
+    int rc = launch_fir_axis0<T>(R, tp, a.vbar, a.vtmp, (int)B2, g.H, (long long)g.W, true, 0,
+                                 nullptr, 0, 2, s);
     if (rc) return rc;
     constexpr size_t bytes = V::bytes;
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        k_velocity_adj2d_h<R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    const cudaError_t attr = ensure_smem<k_velocity_adj2d_h<R, REG>>(bytes);
     if (attr != cudaSuccess) return cuda_status(attr);
     a.vbar = a.vtmp;
     k_velocity_adj2d_h<R, REG>
@@ -189,15 +113,10 @@ int veladj_r(const Grid2& g, const Taps<T>& tp, VelAdjArgs<T> a, cudaStream_t s)
     int rc = veladj_split_r<T, R, REG>(g, tp, a, s);
     if (rc != 1) return rc;
   }
-  {
-    int rc = veladj_stream_r<T, R, REG>(g, tp, a, s);
-    if (rc != 1) return rc;
-  }
   using S = FirSmem<T, R, 2>;
   using V = VelAdjSmem<T, R>;
   constexpr size_t bytes = VelAdjSmem<T, R>::bytes;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      k_velocity_adj2d<T, R, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const cudaError_t attr = ensure_smem<k_velocity_adj2d<T, R, REG>>(bytes);
   if (attr != cudaSuccess) return cuda_status(attr);
   VelAdjMaps m;
   const long long B2 = 2LL * g.B;
@@ -252,48 +171,6 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
   }
 }
 
-template <typename T, int R, bool TR, int EPI>
-int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                int32_t* guard, int guard_stride, int ncomp, cudaStream_t s) {
-  if constexpr (sizeof(T) == 4) {  // fp32: FFMA2 engine, 64 x 64 tiles
-    constexpr size_t bytes = Ax0F32Smem<R>::bytes;
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        k_fir_axis0_f32<R, TR, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (attr != cudaSuccess) return cuda_status(attr);
-    dim3 grid((unsigned)((HW + kA0X - 1) / kA0X), (unsigned)((D + kA0D - 1) / kA0D), (unsigned)V);
-    k_fir_axis0_f32<R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
-                                                               ncomp, tp);
-    return cuda_status(cudaGetLastError());
-  } else {
-  constexpr size_t bytes = Ax0Smem<T, R>::bytes;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      k_fir_axis0<T, R, TR, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (attr != cudaSuccess) return cuda_status(attr);
-  dim3 grid((unsigned)((HW + kAx0X - 1) / kAx0X), (unsigned)((D + kAx0D - 1) / kAx0D),
-            (unsigned)V);
-  k_fir_axis0<T, R, TR, EPI><<<grid, kThreads, bytes, s>>>(in, out, D, HW, guard, guard_stride,
-                                                            ncomp, tp);
-  return cuda_status(cudaGetLastError());
-  }
-}
-
-template <typename T>
-int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
-                     bool transpose, int epi, int32_t* guard, int guard_stride, int ncomp,
-                     cudaStream_t s) {
-  switch (R) {
-#define MR_CASE(RR)                                                                          \
-  case RR:                                                                                   \
-    if (transpose)                                                                           \
-      return fir_axis0_r<T, RR, true, 0>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s);     \
-    if (epi) return fir_axis0_r<T, RR, false, 1>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s); \
-    return fir_axis0_r<T, RR, false, 0>(tp, in, out, V, D, HW, guard, guard_stride, ncomp, s);
-    MR_RADIUS_LIST(MR_CASE)
-#undef MR_CASE
-    default: return MR_EINVAL;
-  }
-}
-
 }  // namespace mr
 
 // One launcher per translation unit (mr_fir_<launcher>_<precision>.cu) so the
@@ -313,12 +190,6 @@ int launch_fir_axis0(int R, const Taps<T>& tp, const T* in, T* out, int V, int D
   template int launch_velocity_adj2d<T>(const Grid2&, int, const Taps<T>&,                      \
                                         const VelAdjArgs<T>&, bool, cudaStream_t);              \
   }
-#define MR_INSTANTIATE_AXIS0(T)                                                                 \
-  namespace mr {                                                                                \
-  template int launch_fir_axis0<T>(int, const Taps<T>&, const T*, T*, int, int, long long, bool, \
-                                   int, int32_t*, int, int, cudaStream_t);                      \
-  }
-
 // Radius groups: the per-radius kernels of the two heavy launchers (velocity,
 // velocity adjoint) are instantiated in mr_fir_<launcher>_<prec>_g<k>.cu (radius
 // r with r % 4 == k) so they compile in parallel; the dispatching translation unit

@@ -1,11 +1,14 @@
 // mr_launch.cuh -- host-side launchers (templated on precision) shared by the
 // translation units.  The FIR-engine launchers (radius dispatch 1..MR_MAX_RADIUS)
 // are defined in mr_fir_impl.cuh and explicitly instantiated per precision in
-// mr_fir_f32.cu / mr_fir_f64.cu so the heavy unrolled kernels compile in parallel.
+// mr_fir_<launcher>_<precision>.cu so the heavy unrolled kernels compile in parallel.
 #pragma once
 
 #include "mr_kernels2d.cuh"
 #include "mr_kernels3d.cuh"
+
+#include <climits>
+#include <cstdlib>
 
 namespace mr {
 
@@ -16,6 +19,25 @@ inline int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return MR_OK;
   g_last_cuda = e;
   return MR_ECUDA;
+}
+
+// Grid of a persistent kernel: resident CTAs per SM (occupancy of `kernel` at
+// `smem` bytes, capped by MR_PERSIST_CTAS_PER_SM when set) x SMs, at most `work`.
+template <typename K>
+inline int persistent_ctas(K kernel, size_t smem, long long work) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem) != cudaSuccess ||
+      per < 1)
+    per = 1;
+  static const int cap = [] {
+    const char* e = getenv("MR_PERSIST_CTAS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0 && per > cap) per = cap;
+  const long long n = (long long)sms * per;
+  return (int)(work < n ? (work < 1 ? 1 : work) : n);
 }
 
 template <typename T>

@@ -23,13 +23,18 @@ from .errors import FieldError, IntegrationDiverged
 MAGNITUDE_GUARD = 1e6  # integrator.py:36
 
 
-def _check_field(t: torch.Tensor, shape, what: str):
-    if tuple(t.shape) != tuple(shape):
+def _check_field(t: torch.Tensor, shape, what: str, like: torch.Tensor | None = None):
+    """Shape, CUDA, contiguity and -- against `like` -- dtype and device: the
+    kernels read raw pointers, so a float64 operand next to float32 ones (or a
+    tensor on another GPU) would otherwise be misread silently."""
+    if shape is not None and tuple(t.shape) != tuple(shape):
         raise FieldError(f"{what}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
     if not t.is_cuda:
         raise FieldError(f"{what}: expected a CUDA tensor")
     if not t.is_contiguous():
         raise FieldError(f"{what}: expected a contiguous tensor")
+    if like is not None and (t.dtype != like.dtype or t.device != like.device):
+        raise FieldError(f"{what}: expected {like.dtype} on {like.device}, got {t.dtype} on {t.device}")
 
 
 @dataclass
@@ -87,12 +92,13 @@ def shoot_forward(traj: DeviceTrajectory, mu: float, weights, stream=None,
     kern = _lib.KernelHandle(weights)
     dt = _lib.dtype_code(traj.I.dtype)
     g = _lib.make_grid(traj.batch, traj.shape)
-    rc = lib.mr_shoot_forward_scheme(
-        dt, g, kern.struct, _lib.SCHEME_CODES[str(scheme)], float(mu), int(traj.n_steps),
-        _lib.ptr(traj.I), _lib.ptr(traj.z),
-        _lib.ptr(traj.v), _lib.ptr(traj.phi), _lib.ptr(traj.guard), _lib.ptr(traj.workspace),
-        _lib.stream_ptr(stream),
-    )
+    with torch.cuda.device(traj.I.device):
+        rc = lib.mr_shoot_forward_scheme(
+            dt, g, kern.struct, _lib.SCHEME_CODES[str(scheme)], float(mu), int(traj.n_steps),
+            _lib.ptr(traj.I), _lib.ptr(traj.z),
+            _lib.ptr(traj.v), _lib.ptr(traj.phi), _lib.ptr(traj.guard), _lib.ptr(traj.workspace),
+            _lib.stream_ptr(stream),
+        )
     _lib.check(rc)
     return traj
 
@@ -152,18 +158,19 @@ def shoot_adjoint(traj: DeviceTrajectory, target: torch.Tensor, lam: float, rho:
     {total, data_term, v_norm, z_norm} [B, 4] (fp64), .flags = non-finite flag [B].
     """
     lib = _lib.load_library()
-    _check_field(target, (traj.batch,) + traj.shape, "target")
+    _check_field(target, (traj.batch,) + traj.shape, "target", like=traj.I)
     if bufs is None:
         bufs = AdjointBuffers(traj.batch, traj.shape, traj.I.dtype, traj.I.device)
     kern = _lib.KernelHandle(weights)
     g = _lib.make_grid(traj.batch, traj.shape)
-    rc = lib.mr_shoot_adjoint_scheme(
-        _lib.dtype_code(traj.I.dtype), g, kern.struct, _lib.SCHEME_CODES[str(scheme)], float(mu),
-        int(traj.n_steps), float(lam),
-        float(rho), _lib.ptr(traj.I), _lib.ptr(traj.z), _lib.ptr(traj.v), _lib.ptr(target),
-        _lib.ptr(bufs.zbar), _lib.ptr(bufs.terms), _lib.ptr(bufs.flags), _lib.ptr(bufs.workspace),
-        _lib.stream_ptr(stream),
-    )
+    with torch.cuda.device(traj.I.device):
+        rc = lib.mr_shoot_adjoint_scheme(
+            _lib.dtype_code(traj.I.dtype), g, kern.struct, _lib.SCHEME_CODES[str(scheme)],
+            float(mu), int(traj.n_steps), float(lam),
+            float(rho), _lib.ptr(traj.I), _lib.ptr(traj.z), _lib.ptr(traj.v), _lib.ptr(target),
+            _lib.ptr(bufs.zbar), _lib.ptr(bufs.terms), _lib.ptr(bufs.flags),
+            _lib.ptr(bufs.workspace), _lib.stream_ptr(stream),
+        )
     _lib.check(rc)
     return bufs
 
@@ -173,12 +180,18 @@ def cost_terms(I0, z0, v0, IT, J, lam, rho, stream=None) -> torch.Tensor:
     lib = _lib.load_library()
     B = I0.shape[0]
     shape = tuple(I0.shape[1:])
+    _check_field(I0, None, "I0")
+    for t, what in ((z0, "z0"), (IT, "I_T"), (J, "target")):
+        _check_field(t, I0.shape, what, like=I0)
+    _check_field(v0, (B, len(shape)) + shape, "v0", like=I0)
     terms = torch.empty((B, 4), dtype=torch.float64, device=I0.device)
     g = _lib.make_grid(B, shape)
-    rc = lib.mr_cost_terms(
-        _lib.dtype_code(I0.dtype), g, float(lam), float(rho), _lib.ptr(I0), _lib.ptr(z0),
-        _lib.ptr(v0), _lib.ptr(IT), _lib.ptr(J), _lib.ptr(terms), None, _lib.stream_ptr(stream),
-    )
+    with torch.cuda.device(I0.device):
+        rc = lib.mr_cost_terms(
+            _lib.dtype_code(I0.dtype), g, float(lam), float(rho), _lib.ptr(I0), _lib.ptr(z0),
+            _lib.ptr(v0), _lib.ptr(IT), _lib.ptr(J), _lib.ptr(terms), None,
+            _lib.stream_ptr(stream),
+        )
     _lib.check(rc)
     return terms
 
@@ -199,12 +212,14 @@ def velocity(I: torch.Tensor, z: torch.Tensor, weights, guard=None, stream=None,
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
-    _check_field(z, I.shape, "momentum")
+    _check_field(I, None, "image")
+    _check_field(z, I.shape, "momentum", like=I)
     v = torch.empty((B, len(shape)) + shape, dtype=I.dtype, device=I.device)
     kern = _lib.KernelHandle(weights)
-    rc = lib.mr_velocity(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), kern.struct,
-                         _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(guard),
-                         _lib.ptr(_split_workspace(I, split)), _lib.stream_ptr(stream))
+    with torch.cuda.device(I.device):
+        rc = lib.mr_velocity(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), kern.struct,
+                             _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(guard),
+                             _lib.ptr(_split_workspace(I, split)), _lib.stream_ptr(stream))
     _lib.check(rc)
     return v
 
@@ -214,12 +229,18 @@ def sl_step(I, z, v, dt, mu, phi=None, stream=None):
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
+    _check_field(I, None, "image")
+    _check_field(z, I.shape, "momentum", like=I)
+    _check_field(v, (B, len(shape)) + shape, "velocity", like=I)
+    if phi is not None:
+        _check_field(phi, (B, len(shape)) + shape, "phi", like=I)
     In = torch.empty_like(I)
     zn = torch.empty_like(z)
     phn = torch.empty_like(phi) if phi is not None else None
-    rc = lib.mr_sl_step(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), float(dt), float(mu),
-                        _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(In), _lib.ptr(zn),
-                        _lib.ptr(phi), _lib.ptr(phn), _lib.stream_ptr(stream))
+    with torch.cuda.device(I.device):
+        rc = lib.mr_sl_step(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), float(dt),
+                            float(mu), _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(In),
+                            _lib.ptr(zn), _lib.ptr(phi), _lib.ptr(phn), _lib.stream_ptr(stream))
     _lib.check(rc)
     return In, zn, phn
 
@@ -229,13 +250,18 @@ def sl_step_adjoint(I, z, v, ibar, zbar, dt, mu, stream=None):
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
+    _check_field(I, None, "image")
+    for t, what in ((z, "momentum"), (ibar, "ibar"), (zbar, "zbar")):
+        _check_field(t, I.shape, what, like=I)
+    _check_field(v, (B, len(shape)) + shape, "velocity", like=I)
     ib = torch.zeros_like(I)
     zb = torch.zeros_like(I)
     vbar = torch.empty_like(v)
-    rc = lib.mr_sl_step_adjoint(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), float(dt),
-                                float(mu), _lib.ptr(I), _lib.ptr(z), _lib.ptr(v), _lib.ptr(ibar),
-                                _lib.ptr(zbar), _lib.ptr(ib), _lib.ptr(zb), _lib.ptr(vbar),
-                                _lib.stream_ptr(stream))
+    with torch.cuda.device(I.device):
+        rc = lib.mr_sl_step_adjoint(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape),
+                                    float(dt), float(mu), _lib.ptr(I), _lib.ptr(z), _lib.ptr(v),
+                                    _lib.ptr(ibar), _lib.ptr(zbar), _lib.ptr(ib), _lib.ptr(zb),
+                                    _lib.ptr(vbar), _lib.stream_ptr(stream))
     _lib.check(rc)
     return ib, zb, vbar
 
@@ -247,11 +273,16 @@ def velocity_adjoint(I, z, vbar, ib, zb, weights, stream=None, split: bool = Tru
     lib = _lib.load_library()
     B = I.shape[0]
     shape = tuple(I.shape[1:])
+    _check_field(I, None, "image")
+    for t, what in ((z, "momentum"), (ib, "ib"), (zb, "zb")):
+        _check_field(t, I.shape, what, like=I)
+    _check_field(vbar, (B, len(shape)) + shape, "vbar", like=I)
     kern = _lib.KernelHandle(weights)
-    rc = lib.mr_velocity_adjoint(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape), kern.struct,
-                                 _lib.ptr(I), _lib.ptr(z), _lib.ptr(vbar), _lib.ptr(ib),
-                                 _lib.ptr(zb), _lib.ptr(_split_workspace(I, split)),
-                                 _lib.stream_ptr(stream))
+    with torch.cuda.device(I.device):
+        rc = lib.mr_velocity_adjoint(_lib.dtype_code(I.dtype), _lib.make_grid(B, shape),
+                                     kern.struct, _lib.ptr(I), _lib.ptr(z), _lib.ptr(vbar),
+                                     _lib.ptr(ib), _lib.ptr(zb),
+                                     _lib.ptr(_split_workspace(I, split)), _lib.stream_ptr(stream))
     _lib.check(rc)
     return ib, zb
 
@@ -261,10 +292,13 @@ def smooth(a: torch.Tensor, weights, adjoint: bool = False, stream=None) -> torc
     lib = _lib.load_library()
     B = a.shape[0]
     shape = tuple(a.shape[1:])
+    _check_field(a, None, "field")
     out = torch.empty_like(a)
     kern = _lib.KernelHandle(weights)
-    rc = lib.mr_smooth(_lib.dtype_code(a.dtype), _lib.make_grid(B, shape), kern.struct,
-                       _lib.ptr(a), _lib.ptr(out), int(bool(adjoint)), _lib.stream_ptr(stream))
+    with torch.cuda.device(a.device):
+        rc = lib.mr_smooth(_lib.dtype_code(a.dtype), _lib.make_grid(B, shape), kern.struct,
+                           _lib.ptr(a), _lib.ptr(out), int(bool(adjoint)),
+                           _lib.stream_ptr(stream))
     _lib.check(rc)
     return out
 
@@ -398,3 +432,179 @@ class GroupedBatchGrad:
 
     def launches_per_run(self) -> int:
         return sum(p.launches_per_run() for p in self.parts)
+
+
+# ---- array-level operators (mr_ops.cu; fields.py:144-262, kernel.py:36-68) ----------
+# Scalar batch [B, *shape], vector batch [B, d, *shape]; any device / dtype the
+# library supports; results on the same device and dtype.
+
+
+def _grid_of(a: torch.Tensor, vector: bool = False):
+    shape = tuple(a.shape[2:]) if vector else tuple(a.shape[1:])
+    if len(shape) not in (2, 3):
+        raise FieldError(f"expected a 2d or 3d grid, got shape {shape}")
+    if vector and a.shape[1] != len(shape):
+        raise FieldError(f"vector batch needs {len(shape)} components, got {a.shape[1]}")
+    return _lib.make_grid(a.shape[0], shape), shape
+
+
+def _prep(*ts):
+    """Check every operand is a contiguous CUDA tensor of one dtype and device."""
+    ref = ts[0]
+    for t in ts:
+        if not t.is_cuda:
+            raise FieldError("expected CUDA tensors")
+        if t.dtype != ref.dtype or t.device != ref.device:
+            raise FieldError(f"operand mismatch: {t.dtype}@{t.device} vs {ref.dtype}@{ref.device}")
+        if not t.is_contiguous():
+            raise FieldError("expected contiguous tensors")
+    return _lib.dtype_code(ref.dtype)
+
+
+def axis_diff(a: torch.Tensor, axis: int, adjoint: bool = False, stream=None) -> torch.Tensor:
+    """np.gradient along grid axis `axis` (fields.py:144-145) or its exact
+    transpose (axis_diff_adjoint, fields.py:148-158)."""
+    lib = _lib.load_library()
+    dt = _prep(a)
+    g, _ = _grid_of(a)
+    out = torch.empty_like(a)
+    with torch.cuda.device(a.device):
+        _lib.check(lib.mr_axis_diff(dt, g, int(axis), _lib.ptr(a), _lib.ptr(out),
+                                    int(bool(adjoint)), _lib.stream_ptr(stream)))
+    return out
+
+
+def gradient(f: torch.Tensor, stream=None) -> torch.Tensor:
+    """gradient_arr (fields.py:161-162): [B, *shape] -> [B, d, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(f)
+    g, shape = _grid_of(f)
+    out = torch.empty((f.shape[0], len(shape)) + shape, dtype=f.dtype, device=f.device)
+    with torch.cuda.device(f.device):
+        _lib.check(lib.mr_gradient(dt, g, _lib.ptr(f), _lib.ptr(out), 0, _lib.stream_ptr(stream)))
+    return out
+
+
+def gradient_adjoint(gbar: torch.Tensor, stream=None) -> torch.Tensor:
+    """gradient_adjoint_arr (fields.py:165-166): [B, d, *shape] -> [B, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(gbar)
+    g, shape = _grid_of(gbar, vector=True)
+    out = torch.empty((gbar.shape[0],) + shape, dtype=gbar.dtype, device=gbar.device)
+    with torch.cuda.device(gbar.device):
+        _lib.check(lib.mr_gradient(dt, g, _lib.ptr(gbar), _lib.ptr(out), 1,
+                                   _lib.stream_ptr(stream)))
+    return out
+
+
+def divergence(v: torch.Tensor, stream=None) -> torch.Tensor:
+    """divergence_arr (fields.py:169-170): [B, d, *shape] -> [B, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(v)
+    g, shape = _grid_of(v, vector=True)
+    out = torch.empty((v.shape[0],) + shape, dtype=v.dtype, device=v.device)
+    with torch.cuda.device(v.device):
+        _lib.check(lib.mr_divergence(dt, g, _lib.ptr(v), _lib.ptr(out), _lib.stream_ptr(stream)))
+    return out
+
+
+def conv1d(a: torch.Tensor, weights, axis: int, adjoint: bool = False, stream=None) -> torch.Tensor:
+    """conv1d_replicate (kernel.py:36-45) along grid axis `axis`, or its exact
+    transpose conv1d_replicate_adjoint (kernel.py:48-68)."""
+    lib = _lib.load_library()
+    dt = _prep(a)
+    g, _ = _grid_of(a)
+    kern = _lib.KernelHandle(weights)
+    out = torch.empty_like(a)
+    with torch.cuda.device(a.device):
+        _lib.check(lib.mr_conv1d(dt, g, kern.struct, int(axis), _lib.ptr(a), _lib.ptr(out),
+                                 int(bool(adjoint)), _lib.stream_ptr(stream)))
+    return out
+
+
+def _bad_flag(device):
+    return torch.zeros((1,), dtype=torch.int32, device=device)
+
+
+def _raise_bad(bad):
+    if int(bad.item()) != 0:
+        raise FieldError("sample coordinates contain non-finite values")  # fields.py:208-209
+
+
+def interpolate(coords: torch.Tensor, a: torch.Tensor, stream=None) -> torch.Tensor:
+    """bilinear_plan + bilinear_apply (fields.py:207-240; trilinear in 3D) of a
+    [B, C, *shape] at absolute coordinates [B, d, *shape] -> [B, C, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(coords, a)
+    g, shape = _grid_of(coords, vector=True)
+    if tuple(a.shape[2:]) != shape or a.shape[0] != coords.shape[0]:
+        raise FieldError("interpolated array and sample grid shapes differ")
+    out = torch.empty_like(a)
+    bad = _bad_flag(a.device)
+    with torch.cuda.device(a.device):
+        _lib.check(lib.mr_interpolate(dt, g, _lib.ptr(coords), _lib.ptr(a), _lib.ptr(out),
+                                      int(a.shape[1]), _lib.ptr(bad), _lib.stream_ptr(stream)))
+    _raise_bad(bad)
+    return out
+
+
+def interpolate_adjoint(coords: torch.Tensor, gbar: torch.Tensor, stream=None) -> torch.Tensor:
+    """bilinear_adjoint_values (fields.py:243-254): [B, *shape] -> [B, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(coords, gbar)
+    g, shape = _grid_of(coords, vector=True)
+    out = torch.empty_like(gbar)
+    bad = _bad_flag(gbar.device)
+    with torch.cuda.device(gbar.device):
+        _lib.check(lib.mr_interpolate_adjoint(dt, g, _lib.ptr(coords), _lib.ptr(gbar),
+                                              _lib.ptr(out), _lib.ptr(bad),
+                                              _lib.stream_ptr(stream)))
+    _raise_bad(bad)
+    return out
+
+
+def interpolate_coord_grad(coords: torch.Tensor, a: torch.Tensor, stream=None) -> torch.Tensor:
+    """bilinear_coord_grad (fields.py:257-262): [B, *shape] -> [B, d, *shape]."""
+    lib = _lib.load_library()
+    dt = _prep(coords, a)
+    g, shape = _grid_of(coords, vector=True)
+    out = torch.empty_like(coords)
+    bad = _bad_flag(a.device)
+    with torch.cuda.device(a.device):
+        _lib.check(lib.mr_interpolate_coord_grad(dt, g, _lib.ptr(coords), _lib.ptr(a),
+                                                 _lib.ptr(out), _lib.ptr(bad),
+                                                 _lib.stream_ptr(stream)))
+    _raise_bad(bad)
+    return out
+
+
+def scheme_step(I, z, v, dt, mu, scheme: str = "semi-lagrangian", phi=None, stream=None):
+    """One transport step of any scheme with an explicit dt -> (I', z', phi' or None)
+    (advect_image_* / continuity_*, integrator.py:133-159)."""
+    lib = _lib.load_library()
+    code = _prep(I, z, v)
+    g, shape = _grid_of(I)
+    In = torch.empty_like(I)
+    zn = torch.empty_like(z)
+    phn = torch.empty_like(phi) if phi is not None else None
+    with torch.cuda.device(I.device):
+        _lib.check(lib.mr_scheme_step(code, g, _lib.SCHEME_CODES[str(scheme)], float(dt),
+                                      float(mu), _lib.ptr(I), _lib.ptr(z), _lib.ptr(v),
+                                      _lib.ptr(In), _lib.ptr(zn), _lib.ptr(phi), _lib.ptr(phn),
+                                      _lib.stream_ptr(stream)))
+    return In, zn, phn
+
+
+REDUCE_DOT, REDUCE_SSD, REDUCE_SUMSQ = 0, 1, 2
+
+
+def reduce(a: torch.Tensor, b: torch.Tensor | None, op: int, stream=None) -> torch.Tensor:
+    """Per-pair dot / ssd / sum of squares (fields.py:285-295) -> float64 [B]."""
+    lib = _lib.load_library()
+    code = _prep(a) if b is None else _prep(a, b)
+    g, _ = _grid_of(a)
+    out = torch.empty((a.shape[0],), dtype=torch.float64, device=a.device)
+    with torch.cuda.device(a.device):
+        _lib.check(lib.mr_reduce(code, g, int(op), _lib.ptr(a), _lib.ptr(b), _lib.ptr(out),
+                                 _lib.stream_ptr(stream)))
+    return out

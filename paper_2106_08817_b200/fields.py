@@ -15,6 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import engine
 from .errors import FieldError
 
 __all__ = [
@@ -24,6 +25,21 @@ __all__ = [
     "VectorField",
     "SampleGrid",
     "identity_coords",
+    "axis_diff",
+    "axis_diff_adjoint",
+    "gradient_arr",
+    "gradient_adjoint_arr",
+    "divergence_arr",
+    "divergence_adjoint_arr",
+    "gradient",
+    "divergence",
+    "BilinearPlan",
+    "bilinear_plan",
+    "bilinear_apply",
+    "bilinear_adjoint_values",
+    "bilinear_coord_grad",
+    "interpolate",
+    "interpolate_vec",
     "dot",
     "ssd",
 ]
@@ -199,14 +215,186 @@ def _require_same_geometry(a, b) -> None:
         raise FieldError(f"geometry mismatch: {a.geometry} vs {b.geometry}")
 
 
+# ---- array-level operators (fields.py:144-262) on the device ----------------------
+#
+# Same names, arguments and array layout as the reference (channel-last vector
+# arrays [*shape, d]).  A numpy operand runs in float64 on the current CUDA device
+# and returns numpy; a torch operand keeps its dtype (float32 / float64) and
+# device and returns torch.  All arithmetic runs in libmorphreg_sm100.so
+# (mr_ops.cu); there is no CPU fallback.
+
+
+def _cuda_device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_dev(a, dtype=None):
+    """(CUDA tensor, is_numpy) for an array-level operand."""
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        if not t.is_floating_point():
+            t = t.to(torch.float64)
+        if dtype is not None:
+            t = t.to(dtype)
+        if not t.is_cuda:
+            t = t.to(_cuda_device())
+        return t.contiguous(), False
+    t = torch.from_numpy(np.array(a, dtype=np.float64, order="C"))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(_cuda_device()), True
+
+
+def _back(t: torch.Tensor, as_numpy: bool):
+    return t.cpu().numpy() if as_numpy else t
+
+
+def _last_to_first(t: torch.Tensor) -> torch.Tensor:
+    return torch.movedim(t, -1, 0).contiguous()
+
+
+def _first_to_last(t: torch.Tensor) -> torch.Tensor:
+    return torch.movedim(t, 0, -1).contiguous()
+
+
+def axis_diff(a, axis: int):
+    """np.gradient along `axis` (fields.py:144-145)."""
+    t, np_in = _to_dev(a)
+    return _back(engine.axis_diff(t[None], axis)[0], np_in)
+
+
+def axis_diff_adjoint(gbar, axis: int):
+    """Exact transpose of axis_diff (fields.py:148-158)."""
+    t, np_in = _to_dev(gbar)
+    return _back(engine.axis_diff(t[None], axis, adjoint=True)[0], np_in)
+
+
+def gradient_arr(f):
+    """fields.py:161-162: [*shape] -> [*shape, d]."""
+    t, np_in = _to_dev(f)
+    return _back(_first_to_last(engine.gradient(t[None])[0]), np_in)
+
+
+def gradient_adjoint_arr(gbar):
+    """fields.py:165-166: [*shape, d] -> [*shape]."""
+    t, np_in = _to_dev(gbar)
+    return _back(engine.gradient_adjoint(_last_to_first(t)[None])[0], np_in)
+
+
+def divergence_arr(v):
+    """fields.py:169-170: [*shape, d] -> [*shape]."""
+    t, np_in = _to_dev(v)
+    return _back(engine.divergence(_last_to_first(t)[None])[0], np_in)
+
+
+def divergence_adjoint_arr(dbar):
+    """fields.py:173-176: [*shape] -> [*shape, d] (axis_diff_adjoint per axis)."""
+    t, np_in = _to_dev(dbar)
+    out = torch.stack([engine.axis_diff(t[None], ax, adjoint=True)[0] for ax in range(t.ndim)])
+    return _back(_first_to_last(out), np_in)
+
+
+def gradient(f: ScalarField) -> VectorField:
+    """Discrete spatial gradient (fields.py:179-181)."""
+    g = engine.gradient(f.tensor.to(_cuda_device())[None].contiguous())[0]
+    return VectorField(f.geometry, g, channel_first=True, _trusted=True)
+
+
+def divergence(v: VectorField) -> ScalarField:
+    """Discrete divergence (fields.py:184-186)."""
+    d = engine.divergence(v.tensor.to(_cuda_device())[None].contiguous())[0]
+    return ScalarField(v.geometry, d, _trusted=True)
+
+
+class BilinearPlan:
+    """fields.py:196-204.  The device plan is the sample coordinates themselves
+    (channel-first [d, *shape] on the GPU): corner indices, fractions and the
+    strict inside masks are formed in registers by every kernel that uses the
+    plan (mr_interpolate*, mr_ops.cu), exactly as bilinear_plan defines them."""
+
+    __slots__ = ("coords", "shape")
+
+    def __init__(self, coords: torch.Tensor, shape):
+        self.coords = coords
+        self.shape = tuple(int(n) for n in shape)
+
+    def __repr__(self) -> str:
+        return f"BilinearPlan(shape={self.shape}, device={self.coords.device})"
+
+
+def bilinear_plan(coords, shape) -> BilinearPlan:
+    """fields.py:207-224: coords [*shape, d] (reference layout) -> plan."""
+    t, _ = _to_dev(coords)
+    shape = tuple(int(n) for n in shape)
+    if tuple(t.shape) != shape + (len(shape),):
+        raise FieldError(f"sample coordinates: expected shape {shape + (len(shape),)}, "
+                         f"got {tuple(t.shape)}")
+    if not bool(torch.isfinite(t).all()):
+        raise FieldError("sample coordinates contain non-finite values")
+    return BilinearPlan(_last_to_first(t), shape)
+
+
+def _plan_coords(p: BilinearPlan, like: torch.Tensor) -> torch.Tensor:
+    return p.coords.to(device=like.device, dtype=like.dtype).contiguous()[None]
+
+
+def bilinear_apply(arr, p: BilinearPlan):
+    """fields.py:235-240 (same term order, bitwise-exact at nodes in float64)."""
+    t, np_in = _to_dev(arr)
+    out = engine.interpolate(_plan_coords(p, t), t[None, None])[0, 0]
+    return _back(out, np_in)
+
+
+def bilinear_adjoint_values(p: BilinearPlan, gbar, shape):
+    """fields.py:243-254: transpose of bilinear_apply w.r.t. the sampled array."""
+    t, np_in = _to_dev(gbar)
+    if tuple(shape) != p.shape:
+        raise FieldError(f"geometry mismatch: {tuple(shape)} vs {p.shape}")
+    out = engine.interpolate_adjoint(_plan_coords(p, t), t[None])[0]
+    return _back(out, np_in)
+
+
+def bilinear_coord_grad(arr, p: BilinearPlan):
+    """fields.py:257-262: per-axis derivative of the interpolated value (tuple)."""
+    t, np_in = _to_dev(arr)
+    out = engine.interpolate_coord_grad(_plan_coords(p, t), t[None])[0]
+    return tuple(_back(out[ax], np_in) for ax in range(out.shape[0]))
+
+
+def interpolate(f: ScalarField, at: SampleGrid) -> ScalarField:
+    """Bilinear interpolation of f at the sample positions, clamped (fields.py:265-269)."""
+    _require_same_geometry(f, at)
+    dev = _cuda_device()
+    a = f.tensor.to(dev)
+    c = at.tensor.to(dev, a.dtype)
+    out = engine.interpolate(c[None].contiguous(), a[None, None].contiguous())[0, 0]
+    return ScalarField(f.geometry, out, _trusted=True)
+
+
+def interpolate_vec(v: VectorField, at: SampleGrid) -> VectorField:
+    """Component-wise bilinear interpolation (fields.py:272-280)."""
+    _require_same_geometry(v, at)
+    dev = _cuda_device()
+    a = v.tensor.to(dev)
+    c = at.tensor.to(dev, a.dtype)
+    out = engine.interpolate(c[None].contiguous(), a[None].contiguous())[0]
+    return VectorField(v.geometry, out, channel_first=True, _trusted=True)
+
+
+def _pair_reduce(f, g, op) -> float:
+    dev = _cuda_device()
+    a = f.tensor.to(dev)
+    b = g.tensor.to(dev, a.dtype)
+    return float(engine.reduce(a[None].contiguous(), b[None].contiguous(), op)[0].item())
+
+
 def dot(f: ScalarField, g: ScalarField) -> float:
-    """L2 inner product (fields.py:285-288)."""
+    """L2 inner product (fields.py:285-288), fp64 device reduction."""
     _require_same_geometry(f, g)
-    return float(np.sum(f.values * g.values))
+    return _pair_reduce(f, g, engine.REDUCE_DOT)
 
 
 def ssd(f: ScalarField, g: ScalarField) -> float:
-    """Half the sum of squared differences (fields.py:291-295)."""
+    """Half the sum of squared differences (fields.py:291-295), fp64 device reduction."""
     _require_same_geometry(f, g)
-    diff = f.values - g.values
-    return 0.5 * float(np.sum(diff * diff))
+    return _pair_reduce(f, g, engine.REDUCE_SSD)

@@ -30,6 +30,10 @@ __all__ = [
     "GeodesicState",
     "GeodesicTrajectory",
     "velocity_from_momentum",
+    "advect_image_euler",
+    "advect_image_sl",
+    "continuity_euler",
+    "continuity_sl",
     "shoot",
     "shoot_lddmm",
     "path_energy",
@@ -82,20 +86,66 @@ class GeodesicTrajectory:
         return self.states[-1].image
 
 
-def _to_device(f, dtype) -> torch.Tensor:
+def _to_device(f, dtype=None) -> torch.Tensor:
+    """A field's tensor on the current CUDA device (dtype None: the field's own)."""
     dev = torch.device("cuda", torch.cuda.current_device())
-    return f.tensor.to(dev, dtype).contiguous()
+    t = f.tensor
+    return t.to(dev, dtype if dtype is not None else t.dtype).contiguous()
 
 
 def velocity_from_momentum(z: ScalarField, image: ScalarField, kernel: GaussianKernel,
-                           dtype=torch.float32) -> VectorField:
+                           dtype=None) -> VectorField:
     """v = -K * (z grad I) (integrator.py:124-130)."""
     if z.geometry != image.geometry:
         raise FieldError("momentum/image geometry mismatch")
     I = _to_device(image, dtype).unsqueeze(0)
-    zz = _to_device(z, dtype).unsqueeze(0)
-    v = engine.velocity(I, zz, kernel.weights)[0]
+    zz = _to_device(z, I.dtype).unsqueeze(0)
+    if len(z.geometry.shape) == 2:
+        v = engine.velocity(I, zz, kernel.weights)[0]
+    else:  # 3D: one-state shoot of the whole-loop entry point (velocity at step 0)
+        traj = engine.allocate_trajectory(1, z.geometry.shape, 1, I.dtype, I.device)
+        traj.I[0].copy_(I)
+        traj.z[0].copy_(zz)
+        engine.shoot_forward(traj, 0.0, kernel.weights)
+        v = traj.v[0, 0]
     return VectorField(z.geometry, v, channel_first=True, _trusted=True)
+
+
+def _single_step(scheme: Scheme, image: ScalarField, v: VectorField, z: ScalarField,
+                 mu: float, dt: float):
+    if not (image.geometry == v.geometry == z.geometry):
+        raise FieldError("image/velocity/momentum geometry mismatch")
+    I = _to_device(image).unsqueeze(0)
+    zz = _to_device(z, I.dtype).unsqueeze(0)
+    vv = _to_device(v, I.dtype).unsqueeze(0)
+    In, zn, _ = engine.scheme_step(I, zz, vv, dt, mu, scheme=scheme.value)
+    return In[0], zn[0]
+
+
+def advect_image_euler(image: ScalarField, v: VectorField, z: ScalarField, mu: float,
+                       dt: float) -> ScalarField:
+    """I + dt(-(grad I . v) + mu z) (integrator.py:133-138)."""
+    In, _ = _single_step(Scheme.EULERIAN, image, v, z, mu, dt)
+    return ScalarField(image.geometry, In, _trusted=True)
+
+
+def advect_image_sl(image: ScalarField, v: VectorField, z: ScalarField, mu: float,
+                    dt: float) -> ScalarField:
+    """B(I) + dt mu z at the feet Id - dt v (integrator.py:141-146)."""
+    In, _ = _single_step(Scheme.SEMI_LAGRANGIAN, image, v, z, mu, dt)
+    return ScalarField(image.geometry, In, _trusted=True)
+
+
+def continuity_euler(z: ScalarField, v: VectorField, dt: float) -> ScalarField:
+    """z - dt div(z v) (integrator.py:149-150)."""
+    _, zn = _single_step(Scheme.EULERIAN, z, v, z, 0.0, dt)
+    return ScalarField(z.geometry, zn, _trusted=True)
+
+
+def continuity_sl(z: ScalarField, v: VectorField, dt: float) -> ScalarField:
+    """B(z)(1 - dt div v) at the feet Id - dt v (integrator.py:153-159)."""
+    _, zn = _single_step(Scheme.SEMI_LAGRANGIAN, z, v, z, 0.0, dt)
+    return ScalarField(z.geometry, zn, _trusted=True)
 
 
 def _run(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig, mu: float) -> GeodesicTrajectory:
@@ -134,15 +184,34 @@ def shoot_lddmm(i0: ScalarField, z0: ScalarField, cfg: ShootingConfig) -> Geodes
 
 
 def path_energy(traj: GeodesicTrajectory, kernel: GaussianKernel, rho: float) -> list:
-    """Per-state ||v_t||_V^2 + rho ||z_t||^2 (integrator.py:280-289) = -<m_t, v_t> + rho|z_t|^2."""
-    if traj.device is None:
-        raise FieldError("path_energy needs a device trajectory from shoot()")
-    dev = traj.device
-    T = dev.n_steps
-    B = dev.batch
-    out = []
-    for k in range(T + 1):
-        terms = engine.cost_terms(dev.I[k], dev.z[k], dev.v[k], dev.I[k], dev.I[k], 1.0, rho)
-        t = terms.cpu().numpy()
-        out.append(float(t[0, 2] + rho * t[0, 3]) if B == 1 else [float(x) for x in t[:, 2] + rho * t[:, 3]])
-    return out
+    """Per-state ||v_t||_V^2 + rho ||z_t||^2 with v built from ``kernel``
+    (integrator.py:280-289): m_t = z_t grad I_t, ||v_t||_V^2 = <m_t, K m_t>.
+
+    All T+1 states run as one batch on the device: the velocity kernels give
+    K m_t = -v_t for the requested kernel and mr_cost_terms reduces
+    -<m_t, v_t> and |z_t|^2 in fp64."""
+    if traj.device is not None:
+        I = traj.device.I
+        z = traj.device.z
+        T1, B = I.shape[0], I.shape[1]
+        I = I.reshape((T1 * B,) + tuple(I.shape[2:]))
+        z = z.reshape((T1 * B,) + tuple(z.shape[2:]))
+    else:
+        I = torch.stack([_to_device(s.image) for s in traj.states])
+        z = torch.stack([_to_device(s.momentum, I.dtype) for s in traj.states])
+        T1, B = I.shape[0], 1
+    shape = tuple(I.shape[1:])
+    if len(shape) == 2:
+        v = engine.velocity(I.contiguous(), z.contiguous(), kernel.weights)
+    else:
+        tr = engine.allocate_trajectory(T1 * B, shape, 1, I.dtype, I.device)
+        tr.I[0].copy_(I)
+        tr.z[0].copy_(z)
+        engine.shoot_forward(tr, 0.0, kernel.weights)
+        v = tr.v[0]
+    terms = engine.cost_terms(I.contiguous(), z.contiguous(), v, I.contiguous(), I.contiguous(),
+                              1.0, rho).cpu().numpy()
+    per = [float(t[2] + rho * t[3]) for t in terms]  # v_norm + rho * z_norm
+    if B == 1:
+        return per
+    return [per[k * B:(k + 1) * B] for k in range(T1)]

@@ -132,7 +132,7 @@ class ShootingCost(torch.autograd.Function):
         traj.z[0].copy_(z0)
         engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
         engine.raise_on_guard(traj)
-        tgt = target.contiguous()
+        tgt = target.to(device=z0.device, dtype=z0.dtype).contiguous()
         terms = engine.cost_terms(traj.I[0], traj.z[0], traj.v[0], traj.I[-1], tgt, lam, rho)
         ctx.traj = traj
         ctx.target = tgt
@@ -167,7 +167,8 @@ def cost_and_grad_batch(source: torch.Tensor, target: torch.Tensor, z0: torch.Te
     traj.I[0].copy_(source)
     traj.z[0].copy_(z0)
     engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
-    bufs = engine.shoot_adjoint(traj, target.contiguous(), lam, rho, cfg.mu, cfg.kernel.weights,
+    tgt = target.to(device=z0.device, dtype=z0.dtype).contiguous()
+    bufs = engine.shoot_adjoint(traj, tgt, lam, rho, cfg.mu, cfg.kernel.weights,
                                 scheme=cfg.scheme.value)
     if raise_on_divergence:
         engine.raise_on_guard(traj)

@@ -97,3 +97,80 @@ def test_guard_bit_order_matches_reference_check_order():
     g[1, 4] = 1
     assert guard_report(g) == (1, 3, "non-finite momentum")
     assert [w for _, w in _lib.GUARD_BITS][0] == "non-finite image"
+
+
+def test_operator_entry_points_validate_without_gpu():
+    """The array-level operators reject bad arguments before any CUDA call."""
+    from paper_2106_08817_b200 import _lib
+
+    lib = _lib.load_library(require_cuda=False)
+    g = _lib.make_grid(1, (8, 8))
+    assert lib.mr_axis_diff(0, g, 2, None, None, 0, None) == 1  # axis out of range (2D)
+    assert b"axis" in lib.mr_last_error()
+    assert lib.mr_conv1d(0, g, _lib.KernelHandle(np.ones(3) / 3).struct, 0, None, None, 0,
+                         None) == 1
+    assert lib.mr_reduce(0, g, 7, None, None, None, None) == 1
+    assert lib.mr_scheme_step(0, g, 9, 0.1, 0.0, None, None, None, None, None, None, None,
+                              None) == 1
+    assert lib.mr_interpolate(0, _lib.make_grid(1, (1, 8)), None, None, None, 1, None,
+                              None) == 1
+
+
+def test_bench_gpus_flag_relaunches_one_rank_per_gpu():
+    """`bench.py --gpus N` outside torchrun execs N ranks."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "4",
+                          "--steps", "2", "--print-launch"], capture_output=True, text=True,
+                         check=True, env={k: v for k, v in os.environ.items()
+                                          if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    cmd = json.loads(out.stdout.strip().splitlines()[-1])["launch"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[cmd.index(os.path.join(REPO, "bench.py")) + 1:][:2] == ["--gpus", "4"]
+
+
+def test_morphreg_shim_exposes_reference_names():
+    """tools/morphreg_shim maps every name the reference's tests import onto the
+    facade (fp64 ShootingConfig); importing needs no GPU."""
+    import importlib
+    import sys
+
+    shim = os.path.join(REPO, "tools", "morphreg_shim")
+    sys.path.insert(0, shim)
+    try:
+        for m in [k for k in sys.modules if k == "morphreg" or k.startswith("morphreg.")]:
+            del sys.modules[m]
+        mr = importlib.import_module("morphreg")
+        import torch
+
+        for name in ("FieldError", "GridGeometry", "ScalarField", "VectorField", "SampleGrid",
+                     "gradient", "divergence", "interpolate", "interpolate_vec", "dot", "ssd",
+                     "GaussianKernel", "smooth_scalar", "smooth_vector", "v_norm_sq", "Scheme",
+                     "ShootingConfig", "GeodesicState", "GeodesicTrajectory",
+                     "IntegrationDiverged", "velocity_from_momentum", "shoot", "shoot_lddmm",
+                     "path_energy", "RegistrationProblem", "CostReport", "cost", "grad",
+                     "OptimizeConfig", "OptimizeResult", "Termination", "optimize",
+                     "default_init"):
+            assert hasattr(mr, name), name
+        fields = importlib.import_module("morphreg.fields")
+        for name in ("axis_diff", "axis_diff_adjoint", "bilinear_adjoint_values",
+                     "bilinear_apply", "bilinear_plan", "identity_coords", "gradient_arr"):
+            assert hasattr(fields, name), name
+        kern = importlib.import_module("morphreg.kernel")
+        for name in ("conv1d_replicate", "conv1d_replicate_adjoint", "smooth_adjoint_arr",
+                     "smooth_arr", "smooth_scalar", "smooth_vector", "v_norm_sq",
+                     "v_norm_sq_arr"):
+            assert hasattr(kern, name), name
+        integ = importlib.import_module("morphreg.integrator")
+        for name in ("advect_image_euler", "advect_image_sl", "continuity_euler",
+                     "continuity_sl"):
+            assert hasattr(integ, name), name
+        cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, 4, 0.0, mr.GaussianKernel(1.0))
+        assert cfg.dtype == torch.float64
+    finally:
+        sys.path.remove(shim)
+        for m in [k for k in sys.modules if k == "morphreg" or k.startswith("morphreg.")]:
+            del sys.modules[m]

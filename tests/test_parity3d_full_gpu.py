@@ -1,0 +1,149 @@
+"""Full-size oracle parity for the 3D BASELINE configs (north_star: "matches the
+CPU oracle ... on all 5 configs").
+
+The oracle (oracle/morphreg_oracle.py, float64 numpy) runs in a process pool on
+the GPU box's host cores while the device runs the same inputs:
+
+- config 4: two full 128^3 pairs, T = 15 -- every per-step I, z, v and dH/dz0;
+- config 5: the full 256^3 volume, the first K5 steps of the T = 50 schedule
+  (dt = 1/50 unchanged; oracle ``shoot(..., n_run=K5)``) -- per-step I, z, v;
+- with MR_FULL_PARITY=1 (slow, minutes of single-core oracle time each):
+  config 3 at its full 160x192x160, T = 20 (shoot + grad), and the config-5
+  recipe at 128^3 with its full T = 50 (shoot + grad).
+
+Inputs are the configs' seeded generators with the guard-calibrated momenta of
+the benchmark (paper_2106_08817_b200.calibrate).  Tolerances are north_star's:
+1e-4 relative L2 per step (fp32 vs the fp64 oracle), 1e-3 on dH/dz0.
+"""
+
+import os
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+K5 = 5  # config-5 prefix steps checked at full size
+FULL = os.environ.get("MR_FULL_PARITY") == "1"
+
+
+def _oracle_job(job):
+    """(name, source, target, z0, T, mu, lam, rho, weights, n_run, with_grad) ->
+    (name, states I/z/v, gradient or None) on one host core."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import morphreg_oracle as O
+
+    name, src, tgt, z0, T, mu, lam, rho, w, n_run, with_grad = job
+    if with_grad:
+        rec = {}
+        g = O.grad(src, tgt, z0, lam, rho, T, mu, w, record=rec)
+        I, z, v, _ = rec["traj"]
+    else:
+        g = None
+        I, z, v, _ = O.shoot(src, z0, T, mu, w, with_phi=False, n_run=n_run)
+    f32 = lambda xs: [np.asarray(x, np.float32) for x in xs]  # noqa: E731  (IPC size)
+    return name, (f32(I), f32(z), f32(v)), g
+
+
+def _calibrated(cfg, **kw):
+    from paper_2106_08817_b200.calibrate import calibrate_no_divergence
+    from paper_2106_08817_b200.synthetic import make_config
+
+    c = make_config(cfg, **kw)
+    calibrate_no_divergence(c)
+    return c
+
+
+def _device(c, b, n_run=None):
+    """fp32 device shoot + adjoint of pair b; returns host copies of the first
+    n_run+1 states (all when None) and dH/dz0."""
+    from paper_2106_08817_b200 import engine
+
+    dt = torch.float32
+    traj = engine.allocate_trajectory(1, c.shape, c.n_steps, dt)
+    traj.I[0].copy_(torch.as_tensor(c.source[b:b + 1], dtype=dt))
+    traj.z[0].copy_(torch.as_tensor(c.z0[b:b + 1], dtype=dt))
+    w = c.weights()
+    engine.shoot_forward(traj, c.mu, w)
+    assert engine.guard_report(traj.guard) is None
+    k = c.n_steps if n_run is None else n_run
+    states = ([traj.I[j, 0].cpu().numpy() for j in range(k + 1)],
+              [traj.z[j, 0].cpu().numpy() for j in range(k + 1)],
+              [traj.v[j, 0].cpu().numpy() for j in range(k + 1)])
+    g = None
+    if n_run is None:
+        J = torch.as_tensor(c.target[b:b + 1], dtype=dt, device="cuda")
+        bufs = engine.shoot_adjoint(traj, J, c.lam, c.rho, c.mu, w)
+        g = bufs.zbar[0].cpu().numpy()
+    del traj
+    torch.cuda.empty_cache()
+    return states, g
+
+
+@pytest.fixture(scope="module")
+def full_size():
+    """Launch every oracle job at once (host process pool), run the device side
+    meanwhile, then collect both."""
+    cases = {}
+    c4 = _calibrated(4, batch=2)
+    for b in range(2):
+        cases[f"cfg4_pair{b}"] = (c4, b, None, True)
+    c5 = _calibrated(5)
+    cases["cfg5_prefix"] = (c5, 0, K5, False)
+    if FULL:
+        cases["cfg3_full"] = (_calibrated(3), 0, None, True)
+        cases["cfg5_128"] = (_calibrated(5, shape=(128, 128, 128)), 0, None, True)
+    jobs = [(name, c.source[b], c.target[b], c.z0[b], c.n_steps, c.mu, c.lam, c.rho,
+             c.weights(), n_run, with_grad) for name, (c, b, n_run, with_grad) in cases.items()]
+    workers = max(1, min(len(jobs), len(os.sched_getaffinity(0))))
+    with ProcessPoolExecutor(workers) as ex:
+        futs = [ex.submit(_oracle_job, j) for j in jobs]
+        dev = {name: _device(c, b, n_run) for name, (c, b, n_run, _) in cases.items()}
+        ora = {}
+        for f in futs:
+            name, states, g = f.result()
+            ora[name] = (states, g)
+    meta = {name: {"offset": c.manifest.get("offset_achieved"), "mu": c.mu, "T": c.n_steps,
+                   "shape": c.shape} for name, (c, _, _, _) in cases.items()}
+    return dev, ora, meta
+
+
+def _check(full_size, name):
+    dev, ora, meta = full_size
+    (dI, dz, dv), dg = dev[name]
+    (oI, oz, ov), og = ora[name]
+    assert len(dI) == len(oI)
+    worst = 0.0
+    for k in range(len(oI)):
+        for a, b, what in ((dI[k], oI[k], "I"), (dz[k], oz[k], "z"), (dv[k], ov[k], "v")):
+            e = rel_l2(a, b)
+            worst = max(worst, e)
+            assert e < 1e-4, (name, what, k, e)
+    eg = None
+    if og is not None:
+        eg = rel_l2(dg, og)
+        assert eg < 1e-3, (name, "grad", eg)
+    print(f"{name}: {meta[name]} worst per-step rel L2 {worst:.2e}, grad rel L2 {eg}")
+
+
+def test_config4_two_full_pairs_match_oracle(full_size):
+    _check(full_size, "cfg4_pair0")
+    _check(full_size, "cfg4_pair1")
+
+
+def test_config5_full_volume_prefix_matches_oracle(full_size):
+    _check(full_size, "cfg5_prefix")
+
+
+@pytest.mark.skipif(not FULL, reason="slow (set MR_FULL_PARITY=1)")
+def test_config3_full_size_matches_oracle(full_size):
+    _check(full_size, "cfg3_full")
+
+
+@pytest.mark.skipif(not FULL, reason="slow (set MR_FULL_PARITY=1)")
+def test_config5_recipe_128_full_T_matches_oracle(full_size):
+    _check(full_size, "cfg5_128")
