@@ -59,6 +59,10 @@ def parse():
     p.add_argument("--e2e-chunks", type=int, default=None,
                    help="pair groups of the host-buffer pipeline (default: the API's choice)")
     p.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
+    p.add_argument("--mu", type=float, default=None,
+                   help="override the config's metamorphosis weight (e.g. --config 5 --mu 0)")
+    p.add_argument("--deterministic", action="store_true",
+                   help="fixed-point adjoint scatters (bitwise run-to-run reproducible)")
     p.add_argument("--print-launch", action="store_true",
                    help="print the multi-rank launch command --gpus N would exec, then exit")
     return p.parse_args()
@@ -185,9 +189,9 @@ def run_ours(args):
     spec = CONFIGS[args.config]
     B_global = spec["batch"]
     pairs = shard(B_global, rank, world)
-    c = make_config(args.config, pairs=pairs)
+    c = make_config(args.config, pairs=pairs, mu=args.mu)
     d = len(c.shape)
-    if (d == 3 and c.mu > 0) or args.scheme != "semi-lagrangian":
+    if d == 3 or args.scheme != "semi-lagrangian":
         # untimed input preparation: keep shoots finite (the explicit
         # Eulerian continuity step is CFL-limited at the SL configs' 1 px/step)
         from paper_2106_08817_b200.calibrate import calibrate_no_divergence
@@ -201,7 +205,8 @@ def run_ours(args):
     # pair groups on concurrent streams (2D batches): FIR and transport kernels overlap
     groups = args.groups if args.groups is not None else (2 if d == 2 and len(pairs) >= 8 else 1)
     bg = engine.GroupedBatchGrad(len(pairs), c.shape, T, c.mu, w, c.lam, c.rho, dtype,
-                                 scheme=args.scheme, groups=groups)
+                                 scheme=args.scheme, groups=groups,
+                                 deterministic=args.deterministic)
     bg.load(torch.as_tensor(c.source, dtype=dtype), torch.as_tensor(c.target, dtype=dtype),
             torch.as_tensor(c.z0, dtype=dtype))
     stream = torch.cuda.current_stream()
@@ -284,7 +289,9 @@ def run_ours(args):
                         + ("" if sl else f", scheme={args.scheme}"),
             "scheme": args.scheme,
             "momentum_scale": c.manifest.get("momentum_scale"),
+            "offset_vox_per_step": c.manifest.get("offset_achieved"),
             "cuda_graph": not args.no_graph,
+            "deterministic": bool(args.deterministic),
             "global_batch": B_global,
             "shape": list(c.shape),
             "n_steps": T,
@@ -404,7 +411,8 @@ def run_e2e(c, args, dtype, world):
     import paper_2106_08817_b200 as mr
 
     cfg = mr.ShootingConfig(mr.Scheme(args.scheme), c.n_steps, c.mu,
-                            mr.GaussianKernel(c.sigma, c.radius))
+                            mr.GaussianKernel(c.sigma, c.radius),
+                            deterministic=args.deterministic)
     src = torch.as_tensor(c.source, dtype=dtype).pin_memory()
     tgt = torch.as_tensor(c.target, dtype=dtype).pin_memory()
     z0 = torch.as_tensor(c.z0, dtype=dtype).pin_memory()
@@ -495,7 +503,7 @@ def run_reference(args):
     # T-independent and a full-T 3D oracle grad takes minutes per pair)
     T_sample = spec["n_steps"] if len(spec["shape"]) == 2 else 1
     P = min(cores, spec["batch"])
-    c = make_config(args.config, batch=P)
+    c = make_config(args.config, batch=P, mu=args.mu)
     w = c.weights()
     tasks = [(c.source[i], c.target[i], c.z0[i], T_sample, c.mu, c.lam, c.rho, w, args.scheme)
              for i in range(P)]

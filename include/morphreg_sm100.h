@@ -136,7 +136,9 @@ int mr_scheme_step(int dtype, mr_grid g, int32_t scheme, double dt, double mu,
  * 2D or 3D grids; scalar batch [B][N], vector batch [B][d][N]. */
 
 /* axis_diff (np.gradient, fields.py:144-145) along `axis`, or its exact
- * transpose axis_diff_adjoint (fields.py:148-158) when adjoint != 0. */
+ * transpose axis_diff_adjoint (fields.py:148-158) when adjoint != 0.
+ * mr_axis_diff, mr_conv1d and mr_reduce also take ndim = 1 (lines; n = {N,1,1}),
+ * as the reference's array operators accept any ndarray. */
 int mr_axis_diff(int dtype, mr_grid g, int32_t axis, const void* a, void* out,
                  int32_t adjoint, void* stream);
 
@@ -210,8 +212,17 @@ int mr_shoot_forward_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme,
                             void* traj_z, void* traj_v, void* phi,
                             int32_t* guard, void* workspace, void* stream);
 
-/* Bytes of device workspace mr_shoot_adjoint needs for grid g. */
+/* Bytes of device workspace mr_shoot_adjoint needs for grid g (includes the
+ * fixed-point accumulators of MR_OPT_DETERMINISTIC and the cost partials). */
 size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g);
+
+/* Option bits of mr_shoot_adjoint_ex.  MR_OPT_DETERMINISTIC: the transport
+ * adjoint scatters accumulate in 64-bit fixed point (order-independent integer
+ * adds, scaled per pair by the step's max |ibar|, |zbar|), so repeated calls on
+ * the same inputs give bitwise-identical gradients -- the reference's replay
+ * promise (optimizer.py:5-7).  Without it the scatters are fp32 /
+ * fp64 atomics (faster; last-bit run-to-run variation). */
+enum { MR_OPT_DETERMINISTIC = 1 };
 
 /* grad() reverse sweep (objective.py:91-174) given a forward trajectory:
  *   zbar0: [B][N] output dH/dz0;  J: [B][N] targets;
@@ -236,14 +247,30 @@ int mr_shoot_adjoint_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme,
                             double* terms, int32_t* flags, void* workspace,
                             void* stream);
 
+/* As mr_shoot_adjoint_scheme, plus `options` (MR_OPT_* bits).
+ * flags[b] bit 1 (value 2): a deterministic-mode contribution was outside the
+ * fixed-point range or non-finite (the facade raises). */
+int mr_shoot_adjoint_ex(int dtype, mr_grid g, mr_kernel k, int32_t scheme,
+                        double mu, int32_t n_steps, double lam, double rho,
+                        const void* traj_I, const void* traj_z,
+                        const void* traj_v, const void* J, void* zbar0,
+                        double* terms, int32_t* flags, void* workspace,
+                        int32_t options, void* stream);
+
+/* Bytes of the optional mr_cost_terms workspace (per-block partials). */
+size_t mr_cost_workspace_bytes(int dtype, mr_grid g);
+
 /* cost() terms (objective.py:71-88) from a trajectory's final image and the
  * initial state: terms double[B][4] = {total, data, v_norm, z_norm}.
  * v_norm is computed as -<m0, v0> (K m0 == -v0, kernel.py:103-108).
- * ibar_seed: nullable [B][N], receives I_T - J (objective.py:107). */
+ * ibar_seed: nullable [B][N], receives I_T - J (objective.py:107).
+ * workspace: nullable (mr_cost_workspace_bytes); the fp64 sums are reduced
+ * in a fixed order either way (deterministic), the workspace spreads them over
+ * many blocks per pair. */
 int mr_cost_terms(int dtype, mr_grid g, double lam, double rho,
                   const void* I0, const void* z0, const void* v0,
                   const void* IT, const void* J, double* terms,
-                  void* ibar_seed, void* stream);
+                  void* ibar_seed, void* workspace, void* stream);
 
 /* Separable replicate-border Gaussian smoothing of a scalar batch
  * (smooth_arr, kernel.py:71-73) and its exact transpose

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libmorphreg_sm100.so")
 MR_F32 = 0
 MR_F64 = 1
 MR_MAX_RADIUS = 32
+MR_OPT_DETERMINISTIC = 1
 
 # Scheme codes (MR_SCHEME_*, include/morphreg_sm100.h) by Scheme value.
 SCHEME_CODES = {"semi-lagrangian": 0, "eulerian": 1, "hybrid": 2}
@@ -46,6 +47,8 @@ EXPORTS = (
     "mr_adjoint_workspace_bytes",
     "mr_shoot_adjoint",
     "mr_shoot_adjoint_scheme",
+    "mr_shoot_adjoint_ex",
+    "mr_cost_workspace_bytes",
     "mr_cost_terms",
     "mr_smooth",
     "mr_scheme_step",
@@ -94,7 +97,13 @@ _SIGNATURES = {
         [_i32, MrGrid, MrKernel, _i32, _d, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
          _vp],
     ),
-    "mr_cost_terms": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mr_shoot_adjoint_ex": (
+        _i32,
+        [_i32, MrGrid, MrKernel, _i32, _d, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+         _i32, _vp],
+    ),
+    "mr_cost_workspace_bytes": (ctypes.c_size_t, [_i32, MrGrid]),
+    "mr_cost_terms": (_i32, [_i32, MrGrid, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_smooth": (_i32, [_i32, MrGrid, MrKernel, _vp, _vp, _i32, _vp]),
     "mr_scheme_step": (_i32, [_i32, MrGrid, _i32, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mr_axis_diff": (_i32, [_i32, MrGrid, _i32, _vp, _vp, _i32, _vp]),

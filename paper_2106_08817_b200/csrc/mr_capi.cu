@@ -214,6 +214,28 @@ static int launch_sl_adjoint2d(const Grid2& g, double dt, double mu, const T* I,
   return cuda_status(cudaGetLastError());
 }
 
+// Deterministic-mode transport adjoint (2D): the generic kernels with fixed-point
+// scatters (SL: k_sl_adjoint2d<T, true>; HYBRID: k_scheme_adj2d<T, true>).
+template <typename T, typename Tail>
+static int launch_adjoint2d_det(int scheme, const Grid2& g, double dt, double mu, const T* I,
+                                const T* z, const T* v, const T* ibar, const T* zbar, T* ib,
+                                T* zb, T* vbar, const Tail& tail, cudaStream_t s,
+                                double reg_lam) {
+  AdjArgs<T> a{I, z, v, ibar, zbar, ib, zb, vbar, (T)dt, (T)(dt * mu), mu != 0.0, (T)reg_lam, g};
+  a.qib = tail.q;
+  a.qzb = tail.q + (long long)g.B * g.N;
+  a.mbits = tail.mbits;
+  a.ovf = tail.ovf;
+  if (scheme == kSchemeSL) {
+    dim3 grid((g.W + kAdjTX - 1) / kAdjTX, (g.H + kAdjRows - 1) / kAdjRows, g.B);
+    k_sl_adjoint2d<T, true><<<grid, kThreads, 0, s>>>(a);
+  } else {
+    dim3 grid((g.W + 31) / 32, (g.H + kNW - 1) / kNW, g.B);
+    k_scheme_adj2d<T, true><<<grid, kThreads, 0, s>>>(a, scheme);
+  }
+  return cuda_status(cudaGetLastError());
+}
+
 // Eulerian / Hybrid transport step and its adjoint (mr_schemes2d.cuh).
 template <typename T>
 static int launch_scheme_step2d(int scheme, const Grid2& g, double dt, double mu, const T* I,
@@ -238,18 +260,25 @@ static int launch_scheme_adj2d(int scheme, const Grid2& g, double dt, double mu,
   return cuda_status(cudaGetLastError());
 }
 
+// Cost-term partials: kCostBlocks per pair in the workspace tail (deterministic
+// block-order reduction); without a workspace one block per pair writes its sums
+// straight into terms (same result bits, slower on large grids).
+constexpr int kCostBlocks = 1024;
+
 template <typename T>
 static int launch_cost_terms2d(const Grid2& g, double lam, double rho, const T* I0, const T* z0,
                                const T* v0, const T* IT, const T* J, double* terms, T* seed,
-                               cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(terms, 0, sizeof(double) * 4 * g.B, s);
-  if (e != cudaSuccess) return MR_ECUDA;
-  CostArgs<T> a{I0, z0, v0, IT, J, seed, terms, g};
+                               cudaStream_t s, double* part = nullptr) {
   // one warp per row: blocks of kNW rows
   long long blocks = (g.H + kNW - 1) / kNW;
-  if (blocks > 1024) blocks = 1024;
+  if (blocks > kCostBlocks) blocks = kCostBlocks;
+  if (!part) {
+    part = terms;
+    blocks = 1;
+  }
+  CostArgs<T> a{I0, z0, v0, IT, J, seed, part, g};
   k_cost_terms2d<T><<<dim3((unsigned)blocks, g.B), kThreads, 0, s>>>(a);
-  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, g.B, lam, rho);
+  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, part, (int)blocks, g.B, lam, rho);
   return cuda_status(cudaGetLastError());
 }
 
@@ -347,21 +376,90 @@ static int shoot_forward(const mr_grid& mg, const mr_kernel& k, int scheme, doub
 template <typename T>
 static int cost_terms3d(const Grid3& g, double lam, double rho, const T* I0, const T* z0,
                         const T* v0, const T* IT, const T* J, double* terms, T* seed,
-                        cudaStream_t s) {
-  if (cudaMemsetAsync(terms, 0, sizeof(double) * 4 * g.B, s) != cudaSuccess) return MR_ECUDA;
+                        cudaStream_t s, double* part = nullptr) {
   long long blocks = (g.N + kThreads * 4 - 1) / (kThreads * 4);
-  if (blocks > 1024) blocks = 1024;
+  if (blocks > kCostBlocks) blocks = kCostBlocks;
+  if (!part) {
+    part = terms;
+    blocks = 1;
+  }
   k_cost_terms3d<T><<<dim3((unsigned)blocks, g.B), kThreads, 0, s>>>(I0, z0, v0, IT, J, seed,
-                                                                      terms, g);
-  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, g.B, lam, rho);
+                                                                      part, g);
+  k_finalize_terms<<<(g.B + 127) / 128, 128, 0, s>>>(terms, part, (int)blocks, g.B, lam, rho);
   return cuda_status(cudaGetLastError());
+}
+
+// ---- adjoint workspace tail (after the per-voxel scalar buffers) -----------------
+// [q accumulators: 2 x B*N u64][mbits: B u64][overflow flag][cost partials: B x kCostBlocks x 4]
+struct AdjTail {
+  unsigned long long* q;
+  unsigned long long* mbits;
+  int* ovf;
+  double* part;
+};
+
+static size_t round256(size_t x) { return (x + 255) / 256 * 256; }
+
+static size_t adjoint_head_bytes(int dtype, const mr_grid& g) {
+  return (size_t)(dtype == MR_F32 ? 4 : 8) * (size_t)scalars(g) * (g.ndim == 3 ? 11 : 8);
+}
+
+static size_t adjoint_tail_bytes(const mr_grid& g) {
+  const size_t S1 = (size_t)scalars(g);
+  return round256(16 * S1) + round256(8 * (size_t)g.batch) + 256 +
+         round256((size_t)g.batch * kCostBlocks * 4 * 8);
+}
+
+static AdjTail adjoint_tail(int dtype, const mr_grid& g, void* ws) {
+  const size_t S1 = (size_t)scalars(g);
+  char* p = static_cast<char*>(ws) + round256(adjoint_head_bytes(dtype, g));
+  AdjTail t;
+  t.q = reinterpret_cast<unsigned long long*>(p);
+  p += round256(16 * S1);
+  t.mbits = reinterpret_cast<unsigned long long*>(p);
+  p += round256(8 * (size_t)g.batch);
+  t.ovf = reinterpret_cast<int*>(p);
+  p += 256;
+  t.part = reinterpret_cast<double*>(p);
+  return t;
+}
+
+static dim3 pair_grid(long long N, int B) {
+  long long nb = (N + 255) / 256;
+  if (nb > 256) nb = 256;
+  return dim3((unsigned)nb, (unsigned)B);
+}
+
+// Deterministic mode, once per step before the scatter: per-pair max |ibar|, |zbar|.
+template <typename T>
+static int det_prepare(const AdjTail& t, const T* ibar, const T* zbar, long long N, int B,
+                       cudaStream_t s) {
+  if (cudaMemsetAsync(t.mbits, 0, sizeof(unsigned long long) * (size_t)B, s) != cudaSuccess)
+    return MR_ECUDA;
+  k_absmax_pair<T><<<pair_grid(N, B), 256, 0, s>>>(ibar, zbar, N, t.mbits);
+  return cuda_status(cudaGetLastError());
+}
+
+// ... and after it: fixed point -> T into the scatter targets (cells reset to 0).
+template <typename T>
+static int det_finish(const AdjTail& t, T* ib, T* zb, long long N, int B, cudaStream_t s) {
+  const long long S1 = N * B;
+  k_fix_to_float<T><<<pair_grid(N, B), 256, 0, s>>>(t.q, ib, N, t.mbits);
+  if (zb) k_fix_to_float<T><<<pair_grid(N, B), 256, 0, s>>>(t.q + S1, zb, N, t.mbits);
+  return cuda_status(cudaGetLastError());
+}
+
+static __global__ void k_det_flags(int32_t* flags, const int* ovf, int B) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && *ovf) flags[b] |= 2;
 }
 
 template <typename T>
 static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>& tp, double mu,
                            int T_, double lam, double rho, const T* I, const T* z, const T* v,
                            const T* J, T* zbar0, double* terms, int32_t* flags, T* w,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool det) {
+  const AdjTail tail = adjoint_tail(sizeof(T) == 4 ? MR_F32 : MR_F64, mg, w);
   const Grid3 g = grid3(mg);
   const double dt = 1.0 / T_;
   const long long S1 = (long long)g.B * g.N;
@@ -374,11 +472,18 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
   Grid2 sl{g.B * 3 * g.D, g.H, g.W, g.HW};
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)g.B, s) != cudaSuccess)
     return check_cuda("memset flags");
-  int rc = cost_terms3d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
+  int rc = cost_terms3d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s, tail.part);
   if (rc) return check_rc(rc, "cost_terms3d");
   if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
+  if (det && (cudaMemsetAsync(tail.q, 0, 16 * (size_t)S1, s) != cudaSuccess ||
+              cudaMemsetAsync(tail.ovf, 0, sizeof(int), s) != cudaSuccess))
+    return check_cuda("memset");
   for (int step = T_ - 1; step >= 0; --step) {
-    if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
+    if (det) {
+      if ((rc = det_prepare<T>(tail, cur, cur + S1, g.N, g.B, s))) return check_rc(rc, "det");
+    } else if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) {
+      return check_cuda("memset");
+    }
     Adj3Args<T> a{};
     a.I = I + step * S1;
     a.z = z + step * S1;
@@ -395,9 +500,17 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
     a.has_mu = mu != 0.0;
     a.reg_lam = (T)(step == 0 ? lam : 0.0);
     a.g = g;
+    a.qib = tail.q;
+    a.qzb = tail.q + S1;
+    a.mbits = tail.mbits;
+    a.ovf = tail.ovf;
     k_divseed3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
-    k_sl_adjoint3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
+    if (det)
+      k_sl_adjoint3d<T, true><<<grid3d(g), kThreads, 0, s>>>(a);
+    else
+      k_sl_adjoint3d<T><<<grid3d(g), kThreads, 0, s>>>(a);
     if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "sl_adjoint3d");
+    if (det && (rc = det_finish<T>(tail, acc, acc + S1, g.N, g.B, s))) return check_rc(rc, "det");
     // ktv = K^T vbar: axis 0 first, then axes 1, 2 per slice (kernel.py:76-79 order)
     rc = launch_fir_axis0<T>(k.radius, tp, vbar, tmp, g.B * 3, g.D, g.HW, true, 0, nullptr, 1, 3, s);
     if (rc) return check_rc(rc, "fir_axis0^T");
@@ -425,6 +538,10 @@ static int shoot_adjoint3d(const mr_grid& mg, const mr_kernel& k, const Taps<T>&
     cur = acc;
     acc = t;
   }
+  if (det) {
+    k_det_flags<<<(g.B + 127) / 128, 128, 0, s>>>(flags, tail.ovf, g.B);
+    if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "det flags");
+  }
   return MR_OK;
 }
 
@@ -432,7 +549,7 @@ template <typename T>
 static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, int scheme, double mu, int T_, double lam,
                          double rho, const void* trI, const void* trz, const void* trv,
                          const void* Jv, void* zbar0, double* terms, int32_t* flags, void* ws,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool det) {
   Taps<T> tp;
   int rc = make_taps<T>(k, tp);
   if (rc) return rc;
@@ -440,7 +557,8 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, int scheme, doub
     return shoot_adjoint3d<T>(mg, k, tp, mu, T_, lam, rho, static_cast<const T*>(trI),
                               static_cast<const T*>(trz), static_cast<const T*>(trv),
                               static_cast<const T*>(Jv), static_cast<T*>(zbar0), terms, flags,
-                              static_cast<T*>(ws), s);
+                              static_cast<T*>(ws), s, det);
+  const AdjTail tail = adjoint_tail(sizeof(T) == 4 ? MR_F32 : MR_F64, mg, ws);
   const Grid2 g = grid2(mg);
   const double dt = 1.0 / T_;
   const T* I = static_cast<const T*>(trI);
@@ -457,20 +575,32 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, int scheme, doub
   T* vtmp = w + 6 * S1;  // 2*S1: axis-0 pass of the split velocity adjoint
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)g.B, s) != cudaSuccess)
     return check_cuda("memset flags");
-  rc = launch_cost_terms2d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s);
+  rc = launch_cost_terms2d<T>(g, lam, rho, I, z, v, I + T_ * S1, J, terms, cur, s, tail.part);
   if (rc) return check_rc(rc, "cost_terms");
   // zbar_T = 0 and the first scatter targets; afterwards the velocity-adjoint
   // kernel of each step zeroes the buffers the next step scatters into
   if (cudaMemsetAsync(cur + S1, 0, sizeof(T) * S1, s) != cudaSuccess) return check_cuda("memset");
   if (cudaMemsetAsync(acc, 0, sizeof(T) * 2 * S1, s) != cudaSuccess) return check_cuda("memset");
+  const bool det_scatter = det && scheme != kSchemeEuler;  // the Eulerian adjoint has no scatter
+  if (det_scatter && (cudaMemsetAsync(tail.q, 0, 16 * (size_t)S1, s) != cudaSuccess ||
+                      cudaMemsetAsync(tail.ovf, 0, sizeof(int), s) != cudaSuccess))
+    return check_cuda("memset");
   for (int step = T_ - 1; step >= 0; --step) {
-    if (scheme == kSchemeSL)
+    if (det_scatter) {
+      if ((rc = det_prepare<T>(tail, cur, cur + S1, g.N, g.B, s))) return check_rc(rc, "det");
+      rc = launch_adjoint2d_det<T>(scheme, g, dt, mu, I + step * S1, z + step * S1,
+                                   v + step * SV, cur, cur + S1, acc, acc + S1, vbar, tail, s,
+                                   step == 0 ? lam : 0.0);
+      if (rc) return check_rc(rc, "sl_adjoint (deterministic)");
+      rc = det_finish<T>(tail, acc, scheme == kSchemeSL ? acc + S1 : nullptr, g.N, g.B, s);
+    } else if (scheme == kSchemeSL) {
       rc = launch_sl_adjoint2d<T>(g, dt, mu, I + step * S1, z + step * S1, v + step * SV, cur,
                                   cur + S1, acc, acc + S1, vbar, s, step == 0 ? lam : 0.0);
-    else
+    } else {
       rc = launch_scheme_adj2d<T>(scheme, g, dt, mu, I + step * S1, z + step * S1,
                                   v + step * SV, cur, cur + S1, acc, acc + S1, vbar, s,
                                   step == 0 ? lam : 0.0);
+    }
     if (rc) return check_rc(rc, "sl_adjoint");
     VelAdjArgs<T> a{};
     a.I = I + step * S1;
@@ -497,6 +627,10 @@ static int shoot_adjoint(const mr_grid& mg, const mr_kernel& k, int scheme, doub
     T* t = cur;
     cur = acc;
     acc = t;
+  }
+  if (det_scatter) {
+    k_det_flags<<<(g.B + 127) / 128, 128, 0, s>>>(flags, tail.ovf, g.B);
+    if ((rc = cuda_status(cudaGetLastError()))) return check_rc(rc, "det flags");
   }
   return MR_OK;
 }
@@ -709,9 +843,12 @@ int mr_shoot_forward_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme, d
 
 size_t mr_adjoint_workspace_bytes(int dtype, mr_grid g) {
   if (validate(dtype, g)) return 0;
-  size_t es = dtype == MR_F32 ? 4 : 8;
-  size_t S1 = (size_t)scalars(g);
-  return es * S1 * (g.ndim == 3 ? 11 : 8);
+  return round256(adjoint_head_bytes(dtype, g)) + adjoint_tail_bytes(g);
+}
+
+size_t mr_cost_workspace_bytes(int dtype, mr_grid g) {
+  if (validate(dtype, g)) return 0;
+  return (size_t)g.batch * kCostBlocks * 4 * sizeof(double);
 }
 
 int mr_shoot_adjoint(int dtype, mr_grid g, mr_kernel k, double mu, int32_t n_steps, double lam,
@@ -727,6 +864,17 @@ int mr_shoot_adjoint_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme, d
                             int32_t n_steps, double lam, double rho, const void* traj_I,
                             const void* traj_z, const void* traj_v, const void* J, void* zbar0,
                             double* terms, int32_t* flags, void* workspace, void* stream) {
+  return mr_shoot_adjoint_ex(dtype, g, k, scheme, mu, n_steps, lam, rho, traj_I, traj_z, traj_v,
+                             J, zbar0, terms, flags, workspace, 0, stream);
+}
+
+int mr_shoot_adjoint_ex(int dtype, mr_grid g, mr_kernel k, int32_t scheme, double mu,
+                        int32_t n_steps, double lam, double rho, const void* traj_I,
+                        const void* traj_z, const void* traj_v, const void* J, void* zbar0,
+                        double* terms, int32_t* flags, void* workspace, int32_t options,
+                        void* stream) {
+  if (options & ~MR_OPT_DETERMINISTIC) return fail(MR_EINVAL, "unknown option bits");
+  const bool det = (options & MR_OPT_DETERMINISTIC) != 0;
   int rc = validate(dtype, g);
   if (rc) return rc;
   if ((rc = validate_scheme(scheme, g))) return rc;
@@ -737,16 +885,17 @@ int mr_shoot_adjoint_scheme(int dtype, mr_grid g, mr_kernel k, int32_t scheme, d
     return fail(MR_EINVAL, "NULL pointer");
   rc = MR_DISPATCH(dtype,
                    shoot_adjoint<float>(g, k, scheme, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
-                                        zbar0, terms, flags, workspace, as_stream(stream)),
+                                        zbar0, terms, flags, workspace, as_stream(stream), det),
                    shoot_adjoint<double>(g, k, scheme, mu, n_steps, lam, rho, traj_I, traj_z, traj_v, J,
-                                         zbar0, terms, flags, workspace, as_stream(stream)));
+                                         zbar0, terms, flags, workspace, as_stream(stream), det));
   if (rc) return rc;
   return check_cuda("mr_shoot_adjoint");
 }
 
 int mr_cost_terms(int dtype, mr_grid g, double lam, double rho, const void* I0, const void* z0,
                   const void* v0, const void* IT, const void* J, double* terms, void* ibar_seed,
-                  void* stream) {
+                  void* workspace, void* stream) {
+  double* part = static_cast<double*>(workspace);
   int rc = validate(dtype, g);
   if (rc) return rc;
   if (!I0 || !z0 || !v0 || !IT || !J || !terms) return fail(MR_EINVAL, "NULL pointer");
@@ -755,22 +904,22 @@ int mr_cost_terms(int dtype, mr_grid g, double lam, double rho, const void* I0, 
     rc = MR_DISPATCH(dtype,
                      cost_terms3d<float>(g3, lam, rho, (const float*)I0, (const float*)z0,
                                          (const float*)v0, (const float*)IT, (const float*)J,
-                                         terms, (float*)ibar_seed, as_stream(stream)),
+                                         terms, (float*)ibar_seed, as_stream(stream), part),
                      cost_terms3d<double>(g3, lam, rho, (const double*)I0, (const double*)z0,
                                           (const double*)v0, (const double*)IT,
                                           (const double*)J, terms, (double*)ibar_seed,
-                                          as_stream(stream)));
+                                          as_stream(stream), part));
     return check_rc(rc, "mr_cost_terms");
   }
   Grid2 g2 = grid2(g);
   rc = MR_DISPATCH(dtype,
                    launch_cost_terms2d<float>(g2, lam, rho, (const float*)I0, (const float*)z0,
                                               (const float*)v0, (const float*)IT, (const float*)J,
-                                              terms, (float*)ibar_seed, as_stream(stream)),
+                                              terms, (float*)ibar_seed, as_stream(stream), part),
                    launch_cost_terms2d<double>(g2, lam, rho, (const double*)I0,
                                                (const double*)z0, (const double*)v0,
                                                (const double*)IT, (const double*)J, terms,
-                                               (double*)ibar_seed, as_stream(stream)));
+                                               (double*)ibar_seed, as_stream(stream), part));
   return check_rc(rc, "mr_cost_terms");
 }
 

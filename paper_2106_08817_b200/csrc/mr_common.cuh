@@ -145,6 +145,98 @@ __device__ __forceinline__ void flush_flags(unsigned flags, int32_t* dst) {
   if (all && (threadIdx.x & 31) == 0 && dst) atomicOr(reinterpret_cast<int*>(dst), (int)all);
 }
 
+// ---- deterministic (order-independent) accumulation ----------------------------
+// With MR_OPT_DETERMINISTIC the adjoint's scatter targets accumulate in 64-bit
+// two's-complement fixed point (red.global.add.u64): integer addition is
+// associative, so the result does not depend on the order in which warps add and
+// every run gives the same bits (the reference's replay promise,
+// optimizer.py:5-7).  Per pair the contributions are scaled by 2^S with
+// S = kFixBits - ilogb(max |input|): 2^-kFixBits relative resolution (finer than
+// an fp32 ulp), and 2^(63 - kFixBits) of headroom for the fan-in of a cell.  A
+// contribution outside the range (or non-finite) raises the overflow flag
+// instead of wrapping silently.
+constexpr int kFixBits = 48;
+
+__device__ __forceinline__ double fix_factor(const unsigned long long* mbits, long long b) {
+  const double m = __longlong_as_double((long long)mbits[b]);
+  if (!(m > 0.0) || !isfinite(m)) return 1.0;
+  return ldexp(1.0, kFixBits - ilogb(m));
+}
+
+__device__ __forceinline__ long long to_fix(double x, double f, unsigned& ovf) {
+  const double y = x * f;
+  if (!(fabs(y) < 7.2e16)) {  // 2^56: 2^7 contributions of that size still fit
+    ovf = 1u;
+    return 0;
+  }
+  return __double2ll_rn(y);
+}
+
+__device__ __forceinline__ void fix_add(unsigned long long* p, long long v) {
+  atomicAdd(p, (unsigned long long)v);
+}
+
+// Warp-merged bilinear-transpose scatter (scatter4_merged) in fixed point: every
+// contribution is converted before any merge, so merged and unmerged sums agree.
+__device__ __forceinline__ void scatter4_merged_fix(unsigned long long* __restrict__ out,
+                                                    long long cell, bool valid, long long W,
+                                                    double f, double ca, double cb, double cc,
+                                                    double cd, unsigned& ovf) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  long long qa = valid ? to_fix(ca, f, ovf) : 0, qb = valid ? to_fix(cb, f, ovf) : 0;
+  const long long qc = valid ? to_fix(cc, f, ovf) : 0, qd = valid ? to_fix(cd, f, ovf) : 0;
+  const long long key = valid ? cell : -4;
+  const long long prev_key = __shfl_up_sync(full, key, 1);
+  const long long next_key = __shfl_down_sync(full, key, 1);
+  const long long pc = __shfl_up_sync(full, qc, 1);
+  const long long pd = __shfl_up_sync(full, qd, 1);
+  if (!valid) return;
+  const bool merge_left = lane > 0 && prev_key >= 0 && prev_key + 1 == key;
+  const bool merged_by_next = lane < 31 && next_key >= 0 && key + 1 == next_key;
+  if (merge_left) {
+    qa += pc;
+    qb += pd;
+  }
+  fix_add(out + cell, qa);
+  fix_add(out + cell + W, qb);
+  if (!merged_by_next) {
+    fix_add(out + cell + 1, qc);
+    fix_add(out + cell + W + 1, qd);
+  }
+}
+
+// Per-pair max |a|, |b| over [B][N] (grid: x blocks per pair, y = pair) as double
+// bits: non-negative doubles order like their bit patterns, so atomicMax is exact.
+template <typename T>
+__global__ void k_absmax_pair(const T* __restrict__ a, const T* __restrict__ b, long long N,
+                              unsigned long long* mbits) {
+  const long long pb = blockIdx.y;
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    m = fmax(m, fabs((double)a[pb * N + i]));
+    if (b) m = fmax(m, fabs((double)b[pb * N + i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(mbits + pb, (unsigned long long)__double_as_longlong(m));
+}
+
+// Fixed-point cells -> T (q * 2^-S of the pair); resets the cells for the next step.
+template <typename T>
+__global__ void k_fix_to_float(unsigned long long* __restrict__ q, T* __restrict__ out,
+                               long long N, const unsigned long long* mbits) {
+  const long long pb = blockIdx.y;
+  const double inv = 1.0 / fix_factor(mbits, pb);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    out[pb * N + i] = (T)((double)(long long)q[pb * N + i] * inv);
+    q[pb * N + i] = 0ull;
+  }
+}
+
 // ---- cp.async (LDGSTS) staging: many loads in flight, no register round trip ----
 
 template <typename T>

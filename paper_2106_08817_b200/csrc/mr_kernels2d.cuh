@@ -743,6 +743,12 @@ struct AdjArgs {
   bool has_mu;
   T reg_lam;  // k = 0 only: vbar -= reg_lam * z grad I (regulariser fold)
   Grid2 g;
+  // deterministic mode (DET kernels): fixed-point scatter targets, per-pair
+  // max |ibar|, |zbar| as double bits, overflow flag
+  unsigned long long* qib;
+  unsigned long long* qzb;
+  const unsigned long long* mbits;
+  int* ovf;
 };
 
 constexpr int kAdjTX = 32, kAdjTY = kThreads / 32;
@@ -780,7 +786,7 @@ __device__ __forceinline__ void scatter4_merged(T* __restrict__ out, long long c
 constexpr int kAdjPix = 1;                       // pixels per thread (rows kAdjTY apart)
 constexpr int kAdjRows = kAdjTY * kAdjPix;        // tile rows
 
-template <typename T>
+template <typename T, bool DET = false>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   __shared__ T s_div[kAdjRows + 2][kAdjTX + 2];  // s = -dt * zbar * B(z), halo 1
   const int H = a.g.H, W = a.g.W;
@@ -870,17 +876,33 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint2d(AdjArgs<T> a) {
   }
 
   // ---- scatters: ib = P^T ibar; zb = P^T (zbar*scale) + dt mu ibar ----
-  T* __restrict__ ibo = a.ib + b * N;
-  T* __restrict__ zbo = a.zb + b * N;
+  if constexpr (DET) {
+    const double f = fix_factor(a.mbits, b);
+    unsigned ovf = 0;
 #pragma unroll
-  for (int k = 0; k < kAdjPix; ++k) {
-    const T fy = py[k].f, fx = px[k].f, wy = T(1) - fy, wx = T(1) - fx;
-    const T g = ibv[k], w = wz[k];
-    scatter4_merged(ibo, c00[k], own[k], (long long)W, wy * wx * g, fy * wx * g, wy * fx * g,
-                    fy * fx * g);
-    scatter4_merged(zbo, c00[k], own[k], (long long)W, wy * wx * w, fy * wx * w, wy * fx * w,
-                    fy * fx * w);
-    if (own[k] && a.has_mu) atomicAdd(zbo + q[k], a.dtmu * g);  // zb = dt*mu*ibar (:133)
+    for (int k = 0; k < kAdjPix; ++k) {
+      const T fy = py[k].f, fx = px[k].f, wy = T(1) - fy, wx = T(1) - fx;
+      const T g = ibv[k], w = wz[k];
+      scatter4_merged_fix(a.qib + b * N, c00[k], own[k], (long long)W, f, wy * wx * g,
+                          fy * wx * g, wy * fx * g, fy * fx * g, ovf);
+      scatter4_merged_fix(a.qzb + b * N, c00[k], own[k], (long long)W, f, wy * wx * w,
+                          fy * wx * w, wy * fx * w, fy * fx * w, ovf);
+      if (own[k] && a.has_mu) fix_add(a.qzb + b * N + q[k], to_fix(a.dtmu * g, f, ovf));
+    }
+    if (ovf) atomicOr(a.ovf, 1);
+  } else {
+    T* __restrict__ ibo = a.ib + b * N;
+    T* __restrict__ zbo = a.zb + b * N;
+#pragma unroll
+    for (int k = 0; k < kAdjPix; ++k) {
+      const T fy = py[k].f, fx = px[k].f, wy = T(1) - fy, wx = T(1) - fx;
+      const T g = ibv[k], w = wz[k];
+      scatter4_merged(ibo, c00[k], own[k], (long long)W, wy * wx * g, fy * wx * g, wy * fx * g,
+                      fy * fx * g);
+      scatter4_merged(zbo, c00[k], own[k], (long long)W, wy * wx * w, fy * wx * w, wy * fx * w,
+                      fy * fx * w);
+      if (own[k] && a.has_mu) atomicAdd(zbo + q[k], a.dtmu * g);  // zb = dt*mu*ibar (:133)
+    }
   }
   __syncthreads();
 
@@ -1454,7 +1476,7 @@ struct CostArgs {
   const T* IT;
   const T* J;
   T* seed;  // nullable: I_T - J
-  double* terms;  // [B][4] (zeroed): {total, data, v_norm, z_norm}
+  double* part;  // [B][gridDim.x][4]: per-block {-, data, v.m, z.z} (reduced by k_finalize_terms)
   Grid2 g;
 };
 
@@ -1501,19 +1523,35 @@ __global__ void __launch_bounds__(kThreads) k_cost_terms2d(CostArgs<T> a) {
       zn += (double)zz * (double)zz;
     }
   }
+  // per-block partials, reduced in block order by k_finalize_terms (deterministic:
+  // no floating-point atomics, so the cost is the same bits on every run)
+  double* out = a.part + ((long long)b * gridDim.x + blockIdx.x) * 4;
   double s;
   s = block_sum(data, red);
-  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 1], 0.5 * s);
+  if (threadIdx.x == 0) out[1] = s;
   s = block_sum(vn, red);
-  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 2], -s);
+  if (threadIdx.x == 0) out[2] = s;
   s = block_sum(zn, red);
-  if (threadIdx.x == 0) atomicAdd(&a.terms[b * 4 + 3], s);
+  if (threadIdx.x == 0) out[3] = s;
 }
 
-static __global__ void k_finalize_terms(double* terms, int B, double lam, double rho) {
+// terms[b] = {total, 0.5 sum data, -sum v.m, sum z.z} from nblk partials per pair,
+// summed in block order; part may alias terms when nblk == 1.
+static __global__ void k_finalize_terms(double* terms, const double* part, int nblk, int B,
+                                        double lam, double rho) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) {
+    double d = 0.0, vn = 0.0, zn = 0.0;
+    for (int k = 0; k < nblk; ++k) {
+      const double* p = part + ((long long)b * nblk + k) * 4;
+      d += p[1];
+      vn += p[2];
+      zn += p[3];
+    }
     double* t = terms + b * 4;
+    t[1] = 0.5 * d;
+    t[2] = -vn;
+    t[3] = zn;
     t[0] = t[1] + lam * (t[2] + rho * t[3]);  // objective.py:87
   }
 }

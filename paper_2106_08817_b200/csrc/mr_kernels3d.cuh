@@ -258,6 +258,10 @@ struct Adj3Args {
   bool has_mu;
   T reg_lam;
   Grid3 g;
+  unsigned long long* qib;  // deterministic mode: fixed-point scatter targets (mr_common.cuh)
+  unsigned long long* qzb;
+  const unsigned long long* mbits;
+  int* ovf;
 };
 
 template <typename T>
@@ -297,7 +301,32 @@ __device__ __forceinline__ void scatter8_merged(T* __restrict__ out, int base, b
   }
 }
 
+// scatter8_merged in fixed point (contributions converted before any merge)
 template <typename T>
+__device__ __forceinline__ void scatter8_merged_fix(unsigned long long* __restrict__ out, int base,
+                                                    bool valid, const Grid3& g, const T w[8],
+                                                    double f, unsigned& ovf) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? base : -4;
+  const int prev_key = __shfl_up_sync(full, key, 1);
+  const int next_key = __shfl_down_sync(full, key, 1);
+  const bool merge_left = lane > 0 && prev_key >= 0 && prev_key + 1 == key;
+  const bool merged_by_next = lane < 31 && next_key >= 0 && key + 1 == next_key;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int off = ((c & 1) ? (int)g.HW : 0) + ((c & 2) ? g.W : 0);
+    const long long lo = valid ? to_fix((double)w[c], f, ovf) : 0;
+    const long long hi = valid ? to_fix((double)w[c | 4], f, ovf) : 0;
+    const long long pr = __shfl_up_sync(full, hi, 1);
+    if (valid) {
+      fix_add(out + base + off, merge_left ? lo + pr : lo);
+      if (!merged_by_next) fix_add(out + base + off + 1, hi);
+    }
+  }
+}
+
+template <typename T, bool DET = false>
 __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
   // Latency-bound gathers: every load (v and its neighbours, ibar/zbar, the 8+8
   // corners of I and z, the s neighbours) is issued before the first scatter, so
@@ -387,17 +416,31 @@ __global__ void __launch_bounds__(kThreads) k_sl_adjoint3d(Adj3Args<T> a) {
     }
   }
 
-  T* __restrict__ ibo = a.ib + b * g.N;
-  T* __restrict__ zbo = a.zb + b * g.N;
   T cw[8];
+  if constexpr (DET) {
+    const double f = fix_factor(a.mbits, b);
+    unsigned ovf = 0;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) cw[c] = w8[c] * ib_;
-  scatter8_merged(ibo, base, own, g, cw);
+    for (int c = 0; c < 8; ++c) cw[c] = w8[c] * ib_;
+    scatter8_merged_fix(a.qib + b * g.N, base, own, g, cw, f, ovf);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) cw[c] = w8[c] * wz;
-  scatter8_merged(zbo, base, own, g, cw);
-  if (!own) return;
-  if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
+    for (int c = 0; c < 8; ++c) cw[c] = w8[c] * wz;
+    scatter8_merged_fix(a.qzb + b * g.N, base, own, g, cw, f, ovf);
+    if (own && a.has_mu) fix_add(a.qzb + b * g.N + q, to_fix((double)(a.dtmu * ib_), f, ovf));
+    if (ovf) atomicOr(a.ovf, 1);
+    if (!own) return;
+  } else {
+    T* __restrict__ ibo = a.ib + b * g.N;
+    T* __restrict__ zbo = a.zb + b * g.N;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cw[c] = w8[c] * ib_;
+    scatter8_merged(ibo, base, own, g, cw);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cw[c] = w8[c] * wz;
+    scatter8_merged(zbo, base, own, g, cw);
+    if (!own) return;
+    if (a.has_mu) atomicAdd(zbo + q, a.dtmu * ib_);
+  }
   if (a.reg_lam != T(0)) {
     T g0, g1, g2;
     grad3(I, q, d, y, x, g, g0, g1, g2);
@@ -484,7 +527,7 @@ __global__ void __launch_bounds__(kThreads) k_cost_terms3d(const T* __restrict__
                                                             const T* __restrict__ v0,
                                                             const T* __restrict__ IT,
                                                             const T* __restrict__ J, T* seed,
-                                                            double* terms, Grid3 g) {
+                                                            double* part, Grid3 g) {
   __shared__ double red[kThreads / 32];
   const int b = blockIdx.y;
   const T* Ib = I0 + b * g.N;
@@ -506,12 +549,13 @@ __global__ void __launch_bounds__(kThreads) k_cost_terms3d(const T* __restrict__
     zn += (double)zz * (double)zz;
   }
   double s;
+  double* out = part + ((long long)b * gridDim.x + blockIdx.x) * 4;  // see k_cost_terms2d
   s = block_sum(data, red);
-  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 1], 0.5 * s);
+  if (threadIdx.x == 0) out[1] = s;
   s = block_sum(vn, red);
-  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 2], -s);
+  if (threadIdx.x == 0) out[2] = s;
   s = block_sum(zn, red);
-  if (threadIdx.x == 0) atomicAdd(&terms[b * 4 + 3], s);
+  if (threadIdx.x == 0) out[3] = s;
 }
 
 }  // namespace mr

@@ -28,16 +28,22 @@ struct OpGrid {
   long long N;
 };
 
+// ndim 1..3 (the reference's array operators accept any ndarray: 1D lines are
+// used by its dense-transpose tests); unused trailing extents are 1.
 static OpGrid op_grid(const mr_grid& g) {
   OpGrid o;
   o.B = g.batch;
   o.d = g.ndim;
-  o.n[0] = g.n[0];
-  o.n[1] = g.n[1];
-  o.n[2] = g.ndim == 3 ? g.n[2] : 1;
+  for (int i = 0; i < 3; ++i) o.n[i] = i < g.ndim ? g.n[i] : 1;
   o.st[2] = 1;
-  o.st[1] = g.ndim == 3 ? o.n[2] : 1;
-  o.st[0] = g.ndim == 3 ? (long long)o.n[1] * o.n[2] : o.n[1];
+  o.st[1] = o.n[2];
+  o.st[0] = (long long)o.n[1] * o.n[2];
+  if (g.ndim == 2) {  // [H][W]: axis 0 stride W, axis 1 stride 1
+    o.st[0] = o.n[1];
+    o.st[1] = 1;
+  } else if (g.ndim == 1) {
+    o.st[0] = 1;
+  }
   o.N = (long long)o.n[0] * o.n[1] * o.n[2];
   return o;
 }
@@ -336,12 +342,13 @@ using namespace mr::ops;
 
 namespace {
 
-int op_validate(int dtype, const mr_grid& g) {
+int op_validate(int dtype, const mr_grid& g, bool allow1d = false) {
   if (dtype != MR_F32 && dtype != MR_F64) return set_error(MR_EINVAL, "dtype must be MR_F32 or MR_F64");
-  if (g.ndim != 2 && g.ndim != 3) return set_error(MR_EINVAL, "ndim must be 2 or 3");
+  if (g.ndim != 2 && g.ndim != 3 && !(allow1d && g.ndim == 1))
+    return set_error(MR_EINVAL, allow1d ? "ndim must be 1, 2 or 3" : "ndim must be 2 or 3");
   if (g.batch < 1) return set_error(MR_EINVAL, "batch must be >= 1");
-  if (g.n[0] < 2 || g.n[1] < 2 || (g.ndim == 3 && g.n[2] < 2))
-    return set_error(MR_EINVAL, "grid must be at least 2x2");
+  for (int i = 0; i < g.ndim; ++i)
+    if (g.n[i] < 2) return set_error(MR_EINVAL, "every axis needs at least 2 samples");
   return MR_OK;
 }
 
@@ -370,7 +377,7 @@ extern "C" {
 
 int mr_axis_diff(int dtype, mr_grid g, int32_t axis, const void* a, void* out, int32_t adjoint,
                  void* stream) {
-  int rc = op_validate(dtype, g);
+  int rc = op_validate(dtype, g, true);
   if (rc) return rc;
   if (axis < 0 || axis >= g.ndim) return set_error(MR_EINVAL, "axis out of range");
   if (!a || !out) return set_error(MR_EINVAL, "NULL field pointer");
@@ -420,7 +427,7 @@ int mr_divergence(int dtype, mr_grid g, const void* v, void* out, void* stream) 
 
 int mr_conv1d(int dtype, mr_grid g, mr_kernel k, int32_t axis, const void* a, void* out,
               int32_t adjoint, void* stream) {
-  int rc = op_validate(dtype, g);
+  int rc = op_validate(dtype, g, true);
   if (rc) return rc;
   if (axis < 0 || axis >= g.ndim) return set_error(MR_EINVAL, "axis out of range");
   if (!a || !out) return set_error(MR_EINVAL, "NULL field pointer");
@@ -495,7 +502,7 @@ int mr_interpolate_coord_grad(int dtype, mr_grid g, const void* coords, const vo
 
 int mr_reduce(int dtype, mr_grid g, int32_t op, const void* a, const void* b, double* out,
               void* stream) {
-  int rc = op_validate(dtype, g);
+  int rc = op_validate(dtype, g, true);
   if (rc) return rc;
   if (op < 0 || op > 2) return set_error(MR_EINVAL, "op must be 0 (dot), 1 (ssd) or 2 (sum of squares)");
   if (!a || !out || (op < 2 && !b)) return set_error(MR_EINVAL, "NULL field pointer");

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_scheme_step2d(StepArgs<T> a, T mu,
 // ibar + G^T(-dt v ibar); HYBRID: bilinear scatter into the zeroed ib_acc).  K4
 // then adds zb += mbar . grad I and ib += G^T(mbar z) -- G^T is linear, so the
 // reference's single G^T(grad_ibar) (objective.py:160-161) splits exactly.
-template <typename T>
+template <typename T, bool DET = false>
 __global__ void __launch_bounds__(kThreads) k_scheme_adj2d(AdjArgs<T> a, int scheme) {
   const int H = a.g.H, W = a.g.W;
   const long long N = a.g.N;
@@ -127,8 +127,15 @@ __global__ void __launch_bounds__(kThreads) k_scheme_adj2d(AdjArgs<T> a, int sch
     const long long c00 = (long long)py.i0 * W + px.i0;
     const T ia = I[c00], ib2 = I[c00 + W], ic = I[c00 + 1], id = I[c00 + W + 1];
     const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
-    scatter4_merged(a.ib + b * N, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_,
-                    wy * fx * ib_, fy * fx * ib_);
+    if constexpr (DET) {
+      unsigned ovf = 0;
+      scatter4_merged_fix(a.qib + b * N, c00, own, (long long)W, fix_factor(a.mbits, b),
+                          wy * wx * ib_, fy * wx * ib_, wy * fx * ib_, fy * fx * ib_, ovf);
+      if (ovf) atomicOr(a.ovf, 1);
+    } else {
+      scatter4_merged(a.ib + b * N, c00, own, (long long)W, wy * wx * ib_, fy * wx * ib_,
+                      wy * fx * ib_, fy * fx * ib_);
+    }
     const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
     const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
     vb0 = -dt * ddy * ib_;

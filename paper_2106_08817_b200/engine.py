@@ -142,8 +142,7 @@ class AdjointBuffers:
         nbytes = lib.mr_adjoint_workspace_bytes(_lib.dtype_code(dtype), g)
         if nbytes == 0:
             raise FieldError(lib.mr_last_error().decode())
-        esize = torch.finfo(dtype).bits // 8
-        self.workspace = torch.empty(nbytes // esize, dtype=dtype, device=device)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
         self.zbar = torch.empty((batch,) + tuple(shape), dtype=dtype, device=device)
         self.terms = torch.empty((batch, 4), dtype=torch.float64, device=device)
         self.flags = torch.empty((batch,), dtype=torch.int32, device=device)
@@ -151,11 +150,14 @@ class AdjointBuffers:
 
 def shoot_adjoint(traj: DeviceTrajectory, target: torch.Tensor, lam: float, rho: float, mu: float,
                   weights, bufs: AdjointBuffers | None = None, stream=None,
-                  scheme: str = "semi-lagrangian") -> AdjointBuffers:
+                  scheme: str = "semi-lagrangian", deterministic: bool = False) -> AdjointBuffers:
     """Reverse sweep of grad() (objective.py:91-174) over a forward trajectory.
 
     Returns the buffers: .zbar = dH/dz0 [B, *shape], .terms = CostReport rows
-    {total, data_term, v_norm, z_norm} [B, 4] (fp64), .flags = non-finite flag [B].
+    {total, data_term, v_norm, z_norm} [B, 4] (fp64), .flags [B] (bit 0: non-finite
+    gradient entry; bit 1: deterministic-mode fixed-point range exceeded).
+    ``deterministic`` selects MR_OPT_DETERMINISTIC: fixed-point scatters, so
+    repeated calls give bitwise-identical results (optimizer.py:5-7).
     """
     lib = _lib.load_library()
     _check_field(target, (traj.batch,) + traj.shape, "target", like=traj.I)
@@ -164,12 +166,13 @@ def shoot_adjoint(traj: DeviceTrajectory, target: torch.Tensor, lam: float, rho:
     kern = _lib.KernelHandle(weights)
     g = _lib.make_grid(traj.batch, traj.shape)
     with torch.cuda.device(traj.I.device):
-        rc = lib.mr_shoot_adjoint_scheme(
+        rc = lib.mr_shoot_adjoint_ex(
             _lib.dtype_code(traj.I.dtype), g, kern.struct, _lib.SCHEME_CODES[str(scheme)],
             float(mu), int(traj.n_steps), float(lam),
             float(rho), _lib.ptr(traj.I), _lib.ptr(traj.z), _lib.ptr(traj.v), _lib.ptr(target),
             _lib.ptr(bufs.zbar), _lib.ptr(bufs.terms), _lib.ptr(bufs.flags),
-            _lib.ptr(bufs.workspace), _lib.stream_ptr(stream),
+            _lib.ptr(bufs.workspace), _lib.MR_OPT_DETERMINISTIC if deterministic else 0,
+            _lib.stream_ptr(stream),
         )
     _lib.check(rc)
     return bufs
@@ -186,10 +189,13 @@ def cost_terms(I0, z0, v0, IT, J, lam, rho, stream=None) -> torch.Tensor:
     _check_field(v0, (B, len(shape)) + shape, "v0", like=I0)
     terms = torch.empty((B, 4), dtype=torch.float64, device=I0.device)
     g = _lib.make_grid(B, shape)
+    code = _lib.dtype_code(I0.dtype)
+    part = torch.empty((lib.mr_cost_workspace_bytes(code, g) // 8,), dtype=torch.float64,
+                       device=I0.device)
     with torch.cuda.device(I0.device):
         rc = lib.mr_cost_terms(
-            _lib.dtype_code(I0.dtype), g, float(lam), float(rho), _lib.ptr(I0), _lib.ptr(z0),
-            _lib.ptr(v0), _lib.ptr(IT), _lib.ptr(J), _lib.ptr(terms), None,
+            code, g, float(lam), float(rho), _lib.ptr(I0), _lib.ptr(z0),
+            _lib.ptr(v0), _lib.ptr(IT), _lib.ptr(J), _lib.ptr(terms), None, _lib.ptr(part),
             _lib.stream_ptr(stream),
         )
     _lib.check(rc)
@@ -312,8 +318,9 @@ class BatchGrad:
     """
 
     def __init__(self, batch, shape, n_steps, mu, weights, lam, rho, dtype=torch.float32,
-                 device=None, scheme: str = "semi-lagrangian"):
+                 device=None, scheme: str = "semi-lagrangian", deterministic: bool = False):
         self.scheme = str(scheme)
+        self.deterministic = bool(deterministic)
         self.traj = allocate_trajectory(batch, shape, n_steps, dtype, device)
         self.target = torch.empty((batch,) + tuple(shape), dtype=dtype,
                                   device=self.traj.I.device)
@@ -330,7 +337,7 @@ class BatchGrad:
     def run(self, stream=None):
         shoot_forward(self.traj, self.mu, self.weights, stream, scheme=self.scheme)
         shoot_adjoint(self.traj, self.target, self.lam, self.rho, self.mu, self.weights,
-                      self.bufs, stream, scheme=self.scheme)
+                      self.bufs, stream, scheme=self.scheme, deterministic=self.deterministic)
         return self.bufs
 
     def capture_graph(self):
@@ -379,12 +386,13 @@ class GroupedBatchGrad:
     """
 
     def __init__(self, batch, shape, n_steps, mu, weights, lam, rho, dtype=torch.float32,
-                 device=None, scheme: str = "semi-lagrangian", groups: int = 2):
+                 device=None, scheme: str = "semi-lagrangian", groups: int = 2,
+                 deterministic: bool = False):
         groups = max(1, min(int(groups), batch))
         bounds = [batch * g // groups for g in range(groups + 1)]
         self.bounds = list(zip(bounds[:-1], bounds[1:]))
         self.parts = [BatchGrad(b1 - b0, shape, n_steps, mu, weights, lam, rho, dtype, device,
-                                scheme) for b0, b1 in self.bounds]
+                                scheme, deterministic) for b0, b1 in self.bounds]
         self.streams = [torch.cuda.Stream(device=device) for _ in self.parts]
         self.mu = float(mu)
         self.n_steps = n_steps
@@ -439,10 +447,10 @@ class GroupedBatchGrad:
 # library supports; results on the same device and dtype.
 
 
-def _grid_of(a: torch.Tensor, vector: bool = False):
+def _grid_of(a: torch.Tensor, vector: bool = False, allow_1d: bool = False):
     shape = tuple(a.shape[2:]) if vector else tuple(a.shape[1:])
-    if len(shape) not in (2, 3):
-        raise FieldError(f"expected a 2d or 3d grid, got shape {shape}")
+    if len(shape) not in ((1, 2, 3) if allow_1d else (2, 3)):
+        raise FieldError(f"expected a {'1d, ' if allow_1d else ''}2d or 3d grid, got shape {shape}")
     if vector and a.shape[1] != len(shape):
         raise FieldError(f"vector batch needs {len(shape)} components, got {a.shape[1]}")
     return _lib.make_grid(a.shape[0], shape), shape
@@ -466,7 +474,7 @@ def axis_diff(a: torch.Tensor, axis: int, adjoint: bool = False, stream=None) ->
     transpose (axis_diff_adjoint, fields.py:148-158)."""
     lib = _lib.load_library()
     dt = _prep(a)
-    g, _ = _grid_of(a)
+    g, _ = _grid_of(a, allow_1d=True)
     out = torch.empty_like(a)
     with torch.cuda.device(a.device):
         _lib.check(lib.mr_axis_diff(dt, g, int(axis), _lib.ptr(a), _lib.ptr(out),
@@ -513,7 +521,7 @@ def conv1d(a: torch.Tensor, weights, axis: int, adjoint: bool = False, stream=No
     transpose conv1d_replicate_adjoint (kernel.py:48-68)."""
     lib = _lib.load_library()
     dt = _prep(a)
-    g, _ = _grid_of(a)
+    g, _ = _grid_of(a, allow_1d=True)
     kern = _lib.KernelHandle(weights)
     out = torch.empty_like(a)
     with torch.cuda.device(a.device):
@@ -602,7 +610,7 @@ def reduce(a: torch.Tensor, b: torch.Tensor | None, op: int, stream=None) -> tor
     """Per-pair dot / ssd / sum of squares (fields.py:285-295) -> float64 [B]."""
     lib = _lib.load_library()
     code = _prep(a) if b is None else _prep(a, b)
-    g, _ = _grid_of(a)
+    g, _ = _grid_of(a, allow_1d=True)
     out = torch.empty((a.shape[0],), dtype=torch.float64, device=a.device)
     with torch.cuda.device(a.device):
         _lib.check(lib.mr_reduce(code, g, int(op), _lib.ptr(a), _lib.ptr(b), _lib.ptr(out),

@@ -48,13 +48,18 @@ class Scheme(str, Enum):
 
 @dataclass(frozen=True)
 class ShootingConfig:
-    """integrator.py:54-69; ``dtype`` selects the device precision (float32 default)."""
+    """integrator.py:54-69.  ``dtype`` selects the device precision (float32
+    default); ``deterministic`` makes grad() bitwise reproducible run to run
+    (fixed-point adjoint scatters, MR_OPT_DETERMINISTIC -- the reference's replay
+    promise, optimizer.py:5-7); the batched engine defaults to the faster
+    atomic scatters."""
 
     scheme: Scheme
     n_steps: int
     mu: float
     kernel: GaussianKernel
     dtype: torch.dtype = field(default=torch.float32, compare=False)
+    deterministic: bool = field(default=True, compare=False)
 
     def __post_init__(self) -> None:
         if self.n_steps < 1:

@@ -108,10 +108,14 @@ def _grad_on(problem: RegistrationProblem, z0: ScalarField,
     cfg = problem.cfg
     J = _to_device(problem.target, cfg.dtype).unsqueeze(0)
     bufs = engine.shoot_adjoint(traj, J, problem.lam, problem.rho, cfg.mu, cfg.kernel.weights,
-                                scheme=cfg.scheme.value)
-    if int(bufs.flags[0].item()) != 0:  # objective.py:171-173
+                                scheme=cfg.scheme.value, deterministic=cfg.deterministic)
+    flag = int(bufs.flags[0].item())
+    if flag & 1:  # objective.py:171-173
         bad = torch.nonzero(~torch.isfinite(bufs.zbar[0]))[0].tolist()
         raise FieldError(f"non-finite gradient entry at pixel {tuple(bad)}")
+    if flag & 2:
+        raise FieldError("deterministic adjoint: contribution outside the fixed-point range "
+                         "(non-finite adjoint state)")
     return ScalarField(z0.geometry, bufs.zbar[0], _trusted=True)
 
 
@@ -143,7 +147,7 @@ class ShootingCost(torch.autograd.Function):
     def backward(ctx, grad_out):
         cfg, lam, rho = ctx.params
         bufs = engine.shoot_adjoint(ctx.traj, ctx.target, lam, rho, cfg.mu, cfg.kernel.weights,
-                                    scheme=cfg.scheme.value)
+                                    scheme=cfg.scheme.value, deterministic=cfg.deterministic)
         scale = grad_out.to(bufs.zbar.dtype).view((-1,) + (1,) * (bufs.zbar.ndim - 1))
         ctx.traj = None
         return bufs.zbar * scale, None, None, None, None, None
@@ -169,7 +173,7 @@ def cost_and_grad_batch(source: torch.Tensor, target: torch.Tensor, z0: torch.Te
     engine.shoot_forward(traj, cfg.mu, cfg.kernel.weights, scheme=cfg.scheme.value)
     tgt = target.to(device=z0.device, dtype=z0.dtype).contiguous()
     bufs = engine.shoot_adjoint(traj, tgt, lam, rho, cfg.mu, cfg.kernel.weights,
-                                scheme=cfg.scheme.value)
+                                scheme=cfg.scheme.value, deterministic=cfg.deterministic)
     if raise_on_divergence:
         engine.raise_on_guard(traj)
     return bufs.zbar, bufs.terms, traj.guard
@@ -243,7 +247,8 @@ def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunk
             engine.shoot_forward(trajs[g], cfg.mu, w, stream=s, scheme=cfg.scheme.value)
             s.wait_event(ev_J[g])
             bufs = engine.shoot_adjoint(trajs[g], tgts[g], lam, rho, cfg.mu, w, stream=s,
-                                        scheme=cfg.scheme.value)
+                                        scheme=cfg.scheme.value,
+                                        deterministic=cfg.deterministic)
             keep.append(bufs)
             zbar_h[a:b].copy_(bufs.zbar, non_blocking=True)
             terms_h[a:b].copy_(bufs.terms, non_blocking=True)

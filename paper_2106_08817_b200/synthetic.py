@@ -247,19 +247,25 @@ def _stress_pair(seed: int, shape, spec):
 
 
 def make_config(idx: int, seed: int = 0, batch: int | None = None, pairs=None,
-                shape=None) -> ConfigData:
+                shape=None, mu: float | None = None) -> ConfigData:
     """Inputs of BASELINE config ``idx`` (1..5).
 
     ``batch`` truncates a batched config to its first pairs; ``pairs`` selects
     explicit pair indices (per-rank sharding: pair p uses seed ``seed + p``).
     ``shape`` overrides the grid (reduced-size parity cases of the same recipe).
+    ``mu`` overrides the metamorphosis weight (e.g. the mu = 0 LDDMM variant of
+    config 5, which stays finite at the nominal 3 vox/step offset).
     """
-    spec = CONFIGS[idx]
+    spec = dict(CONFIGS[idx])
+    if mu is not None:
+        spec["mu"] = float(mu)
+        spec["name"] = spec["name"] + f"_mu{float(mu):g}"
     shp = tuple(shape) if shape is not None else spec["shape"]
     if pairs is None:
         pairs = list(range(batch if batch is not None else spec["batch"]))
     manifest = {"config": idx, "seed": seed, "pairs": list(pairs), "shape": list(shp),
-                "ambiguities": "SURVEY.md Appendix C", "offset_nominal": spec.get("offset")}
+                "ambiguities": "SURVEY.md Appendix C", "offset_nominal": spec.get("offset"),
+                "mu": spec["mu"]}
     if idx not in CONFIGS:
         raise ValueError(f"unknown config {idx}")
 

@@ -49,8 +49,13 @@ def test_library_rejects_bad_arguments_without_gpu():
     g = _lib.make_grid(1, (8, 8))
     k = _lib.MrKernel()
     k.radius = 40
-    assert lib.mr_adjoint_workspace_bytes(0, g) == 8 * 8 * 8 * 4
-    assert lib.mr_adjoint_workspace_bytes(1, g) == 8 * 8 * 8 * 8
+    # 8 scalars per pixel, then the tail: fixed-point accumulators (16 B/px), the
+    # per-pair max, the overflow flag and the cost partials (1024 blocks x 4 fp64)
+    r = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    tail = r(16 * 64) + r(8) + 256 + r(1024 * 4 * 8)
+    assert lib.mr_adjoint_workspace_bytes(0, g) == r(8 * 8 * 8 * 4) + tail
+    assert lib.mr_adjoint_workspace_bytes(1, g) == r(8 * 8 * 8 * 8) + tail
+    assert lib.mr_cost_workspace_bytes(0, g) == 1024 * 4 * 8
     with pytest.raises(Exception):
         _lib.KernelHandle(np.ones(81) / 81)  # radius 40 > MR_MAX_RADIUS
 

@@ -11,7 +11,7 @@ from conftest import load_golden, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(9, 7), (2, 5), (6, 5, 4), (2, 3, 7)]
+SHAPES = [(9, 7), (2, 5), (6, 5, 4), (2, 3, 7), (11,), (2,)]
 
 
 def _O():
@@ -56,7 +56,7 @@ def test_axis_diff_adjoint_is_dense_transpose():
         assert np.allclose(F.axis_diff_adjoint(g, ax).ravel(), mat.T @ g.ravel(), atol=1e-14)
 
 
-@pytest.mark.parametrize("shape", SHAPES, ids=str)
+@pytest.mark.parametrize("shape", SHAPES[:4], ids=str)
 def test_gradient_divergence_and_adjoints(shape):
     from paper_2106_08817_b200 import fields as F
 
@@ -86,7 +86,8 @@ def test_field_gradient_divergence_match_reference_goldens():
 
 
 @pytest.mark.parametrize("shape,sigma,radius", [((12, 9), 1.5, None), ((5, 7), 2.0, 9),
-                                                ((6, 5, 8), 1.0, 3), ((2, 3), 1.0, 4)], ids=str)
+                                                ((6, 5, 8), 1.0, 3), ((2, 3), 1.0, 4),
+                                                ((16,), 2.0, None), ((3,), 1.0, None)], ids=str)
 def test_conv1d_and_transpose(shape, sigma, radius):
     from paper_2106_08817_b200 import kernel as K
 
@@ -231,9 +232,9 @@ def test_path_energy_honours_its_kernel(dtype):
     import paper_2106_08817_b200 as mr
 
     O = _O()
-    g = load_golden("shoot_H_100x90_r9.npz")
+    g = load_golden("shoot_E_40x33.npz")
     T, mu = int(g["n_steps"]), float(g["mu"])
-    k_shoot = mr.GaussianKernel(3.0)
+    k_shoot = mr.GaussianKernel(float(g["sigma"]), int(g["radius"]))
     k_shoot.weights = g["weights"]
     cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, T, mu, k_shoot, dtype=dtype)
     traj = mr.shoot(mr.ScalarField.from_array(g["source"]), mr.ScalarField.from_array(g["z0"]),

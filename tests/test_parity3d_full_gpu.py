@@ -7,6 +7,9 @@ the GPU box's host cores while the device runs the same inputs:
 - config 4: two full 128^3 pairs, T = 15 -- every per-step I, z, v and dH/dz0;
 - config 5: the full 256^3 volume, the first K5 steps of the T = 50 schedule
   (dt = 1/50 unchanged; oracle ``shoot(..., n_run=K5)``) -- per-step I, z, v;
+- config 5 with mu = 0 (LDDMM; finite at the nominal ~3 vox/step, so the
+  out-of-cell gathers and scatter contention are exercised): the full-volume
+  prefix, and the full T = 50 shoot + dH/dz0 on a 96^3 grid of the recipe;
 - with MR_FULL_PARITY=1 (slow, minutes of single-core oracle time each):
   config 3 at its full 160x192x160, T = 20 (shoot + grad), and the config-5
   recipe at 128^3 with its full T = 50 (shoot + grad).
@@ -94,6 +97,10 @@ def full_size():
         cases[f"cfg4_pair{b}"] = (c4, b, None, True)
     c5 = _calibrated(5)
     cases["cfg5_prefix"] = (c5, 0, K5, False)
+    # mu = 0 variant: finite at the nominal 3 vox/step (out-of-cell gathers, scatter
+    # contention): the full volume's prefix, and the full T = 50 shoot + grad at 96^3
+    cases["cfg5_mu0_prefix"] = (_calibrated(5, mu=0.0), 0, K5, False)
+    cases["cfg5_mu0_96"] = (_calibrated(5, mu=0.0, shape=(96, 96, 96)), 0, None, True)
     if FULL:
         cases["cfg3_full"] = (_calibrated(3), 0, None, True)
         cases["cfg5_128"] = (_calibrated(5, shape=(128, 128, 128)), 0, None, True)
@@ -137,6 +144,15 @@ def test_config4_two_full_pairs_match_oracle(full_size):
 
 def test_config5_full_volume_prefix_matches_oracle(full_size):
     _check(full_size, "cfg5_prefix")
+
+
+def test_config5_lddmm_variant_at_nominal_offset_matches_oracle(full_size):
+    """mu = 0: ~3 vox per-step back-traces (offset asserted), full-volume prefix and
+    the full T = 50 shoot + gradient at 96^3."""
+    _, _, meta = full_size
+    assert min(meta["cfg5_mu0_prefix"]["offset"]) > 2.0, meta["cfg5_mu0_prefix"]
+    _check(full_size, "cfg5_mu0_prefix")
+    _check(full_size, "cfg5_mu0_96")
 
 
 @pytest.mark.skipif(not FULL, reason="slow (set MR_FULL_PARITY=1)")
