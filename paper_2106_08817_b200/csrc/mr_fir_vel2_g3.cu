@@ -1,0 +1,5 @@
+#include "mr_fir_impl.cuh"
+#include "mr_vel2d.cuh"
+namespace mr {
+MR_RADIUS_GROUP3(MR_VEL2_INST)
+}

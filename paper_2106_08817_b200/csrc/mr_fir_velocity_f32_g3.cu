@@ -1,4 +1,7 @@
 #include "mr_fir_impl.cuh"
 namespace mr {
+MR_RADIUS_LIST(MR_VEL2_EXTERN)
+}
+namespace mr {
 MR_RADIUS_GROUP3(MR_VEL_INST_F32)
 }
