@@ -13,11 +13,11 @@ inline dim3 fir_grid(int W, int H, int B, int tx, int ty) {
 }
 
 
-// Column-pass-first fp32 velocity (mr_vel2d.cuh, instantiated in mr_fir_vel2_g*.cu);
-// returns 1 when not applicable.
+// Register-window fp32 velocity around a transposed intermediate (mr_vel2d.cuh,
+// instantiated in mr_fir_vel2_g*.cu); returns 1 when not applicable.
 template <int R>
-int launch_vel2d_colfirst(const Grid2& g, const Taps<float>& tp, const float* I, const float* z,
-                          float* v, int32_t* guard, int guard_stride, float* ws, cudaStream_t s);
+int launch_vel2d_fast(const Grid2& g, const Taps<float>& tp, const float* I, const float* z,
+                      float* v, int32_t* guard, int guard_stride, float* ws, cudaStream_t s);
 
 // Split velocity (fp32, scratch given): product +
 // axis-1 FIR per tile (k_velocity2d_h) into a.vtmp, then the axis-0 FIR over whole
@@ -32,7 +32,7 @@ int velocity_split_r(const Grid2& g, const Taps<T>& tp, VelArgs<T> a, cudaStream
     if (!a.vtmp) return 1;
     static const bool classic = getenv("MR_VEL_CLASSIC") != nullptr;  // A/B switch
     if (!classic) {
-      int rc = launch_vel2d_colfirst<R>(g, tp, a.I, a.z, a.v, a.guard, a.guard_stride, a.vtmp, s);
+      int rc = launch_vel2d_fast<R>(g, tp, a.I, a.z, a.v, a.guard, a.guard_stride, a.vtmp, s);
       if (rc != 1) return rc;
     }
     CUtensorMap mI, mZ;
@@ -219,9 +219,9 @@ int launch_velocity_adj2d(const Grid2& g, int R, const Taps<T>& tp, const VelAdj
   PFX template int veladj_r<T, RR, false>(const Grid2&, const Taps<T>&, VelAdjArgs<T>,          \
                                           cudaStream_t);
 #define MR_VEL2_DECL(PFX, RR)                                                                  \
-  PFX template int launch_vel2d_colfirst<RR>(const Grid2&, const Taps<float>&, const float*,     \
-                                             const float*, float*, int32_t*, int, float*,        \
-                                             cudaStream_t);
+  PFX template int launch_vel2d_fast<RR>(const Grid2&, const Taps<float>&, const float*,         \
+                                         const float*, float*, int32_t*, int, float*,            \
+                                         cudaStream_t);
 #define MR_VEL2_EXTERN(RR) MR_VEL2_DECL(extern, RR)
 #define MR_VEL2_INST(RR) MR_VEL2_DECL(, RR)
 #define MR_VEL_EXTERN_F32(RR) MR_VELOCITY_R_DECL(extern, float, RR)
