@@ -308,41 +308,64 @@ def divergence(v: VectorField) -> ScalarField:
 
 class BilinearPlan:
     """fields.py:196-204.  The device plan is the sample coordinates themselves
-    (channel-first [d, *shape] on the GPU): corner indices, fractions and the
+    (channel-first [d, *sample_shape] on the GPU): corner indices, fractions and the
     strict inside masks are formed in registers by every kernel that uses the
-    plan (mr_interpolate*, mr_ops.cu), exactly as bilinear_plan defines them."""
+    plan (mr_interpolate*, mr_ops.cu), exactly as bilinear_plan defines them.
+    ``shape`` is the shape of the sampled array; the sample positions may form any
+    other grid (the kernels take one sample per array cell, so other sample counts
+    run as ceil(M / N) array-shaped batches, padded with samples that are dropped)."""
 
-    __slots__ = ("coords", "shape")
+    __slots__ = ("coords", "shape", "sample_shape")
 
     def __init__(self, coords: torch.Tensor, shape):
         self.coords = coords
         self.shape = tuple(int(n) for n in shape)
+        self.sample_shape = tuple(coords.shape[1:])
 
     def __repr__(self) -> str:
-        return f"BilinearPlan(shape={self.shape}, device={self.coords.device})"
+        return (f"BilinearPlan(shape={self.shape}, samples={self.sample_shape}, "
+                f"device={self.coords.device})")
 
 
 def bilinear_plan(coords, shape) -> BilinearPlan:
-    """fields.py:207-224: coords [*shape, d] (reference layout) -> plan."""
+    """fields.py:207-224: coords [..., d] (reference layout, any sample grid) -> plan."""
     t, _ = _to_dev(coords)
     shape = tuple(int(n) for n in shape)
-    if tuple(t.shape) != shape + (len(shape),):
-        raise FieldError(f"sample coordinates: expected shape {shape + (len(shape),)}, "
-                         f"got {tuple(t.shape)}")
+    if t.ndim < 2 or t.shape[-1] != len(shape):
+        raise FieldError(f"sample coordinates: expected [..., {len(shape)}], got {tuple(t.shape)}")
     if not bool(torch.isfinite(t).all()):
         raise FieldError("sample coordinates contain non-finite values")
     return BilinearPlan(_last_to_first(t), shape)
 
 
 def _plan_coords(p: BilinearPlan, like: torch.Tensor) -> torch.Tensor:
-    return p.coords.to(device=like.device, dtype=like.dtype).contiguous()[None]
+    """[nb, d, *shape] coordinate batches of the plan (nb = 1 when the sample grid is
+    the array grid)."""
+    c = p.coords.to(device=like.device, dtype=like.dtype)
+    if p.sample_shape == p.shape:
+        return c.contiguous()[None]
+    d, n = len(p.shape), int(np.prod(p.shape))
+    m = int(np.prod(p.sample_shape))
+    nb = max(1, -(-m // n))
+    flat = torch.zeros((d, nb * n), dtype=c.dtype, device=c.device)
+    flat[:, :m] = c.reshape(d, m)
+    return flat.view((d, nb) + p.shape).transpose(0, 1).contiguous()
+
+
+def _to_samples(p: BilinearPlan, out: torch.Tensor) -> torch.Tensor:
+    """[nb, *shape] kernel output -> [*sample_shape]."""
+    if p.sample_shape == p.shape:
+        return out[0]
+    m = int(np.prod(p.sample_shape))
+    return out.reshape(-1)[:m].view(p.sample_shape)
 
 
 def bilinear_apply(arr, p: BilinearPlan):
     """fields.py:235-240 (same term order, bitwise-exact at nodes in float64)."""
     t, np_in = _to_dev(arr)
-    out = engine.interpolate(_plan_coords(p, t), t[None, None])[0, 0]
-    return _back(out, np_in)
+    c = _plan_coords(p, t)
+    a = t[None, None].expand((c.shape[0], 1) + tuple(t.shape)).contiguous()
+    return _back(_to_samples(p, engine.interpolate(c, a)[:, 0]), np_in)
 
 
 def bilinear_adjoint_values(p: BilinearPlan, gbar, shape):
@@ -350,15 +373,23 @@ def bilinear_adjoint_values(p: BilinearPlan, gbar, shape):
     t, np_in = _to_dev(gbar)
     if tuple(shape) != p.shape:
         raise FieldError(f"geometry mismatch: {tuple(shape)} vs {p.shape}")
-    out = engine.interpolate_adjoint(_plan_coords(p, t), t[None])[0]
-    return _back(out, np_in)
+    c = _plan_coords(p, t)
+    if p.sample_shape == p.shape:
+        g = t[None]
+    else:
+        g = torch.zeros((c.shape[0] * int(np.prod(p.shape)),), dtype=t.dtype, device=t.device)
+        g[:t.numel()] = t.reshape(-1)
+        g = g.view((c.shape[0],) + p.shape)
+    return _back(engine.interpolate_adjoint(c, g.contiguous()).sum(dim=0), np_in)
 
 
 def bilinear_coord_grad(arr, p: BilinearPlan):
     """fields.py:257-262: per-axis derivative of the interpolated value (tuple)."""
     t, np_in = _to_dev(arr)
-    out = engine.interpolate_coord_grad(_plan_coords(p, t), t[None])[0]
-    return tuple(_back(out[ax], np_in) for ax in range(out.shape[0]))
+    c = _plan_coords(p, t)
+    a = t[None].expand((c.shape[0],) + tuple(t.shape)).contiguous()
+    out = engine.interpolate_coord_grad(c, a)
+    return tuple(_back(_to_samples(p, out[:, ax]), np_in) for ax in range(out.shape[1]))
 
 
 def interpolate(f: ScalarField, at: SampleGrid) -> ScalarField:

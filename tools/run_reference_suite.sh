@@ -20,6 +20,7 @@ case "${1:-run}" in
     cd "$DST"
     PYTHONPATH="$ROOT/tools/morphreg_shim:$ROOT" python -m pytest -p no:cacheprovider -q \
       -o addopts="" --rootdir "$DST" \
-      test_fields.py test_kernel.py test_integrator.py test_objective.py test_optimizer.py "$@"
+      test_fields.py test_kernel.py test_integrator.py test_objective.py test_optimizer.py \
+      test_synthetic.py test_io_cli.py test_acceptance.py "$@"
     ;;
 esac
