@@ -186,8 +186,8 @@ int mr_reduce(int dtype, mr_grid g, int32_t op, const void* a, const void* b,
 
 /* Bytes of device workspace mr_shoot_forward uses: 3 scalars per voxel in 3D,
  * where the separable smoothing round-trips through it (required); 2 scalars
- * per pixel in 2D, where it holds the axis-1 pass of the split fp32 velocity
- * (optional: NULL keeps the single-kernel velocity). */
+ * per pixel in 2D, where it holds the transposed intermediate hT of the fp32 velocity
+ * (k_vel_a / k_vel_b; optional: NULL keeps the single-kernel velocity). */
 size_t mr_forward_workspace_bytes(int dtype, mr_grid g);
 
 /* shoot() for Scheme.SEMI_LAGRANGIAN (integrator.py:163-219), every pair of

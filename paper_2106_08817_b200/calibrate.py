@@ -6,7 +6,7 @@ metamorphic shoots (mu > 0) run away: max|z_t| passes the 1e6 guard
 (integrator.py:113-118).  Below the guard there is a band where the shoot stays
 finite but the momentum grows by 10^2-10^6 and the dynamics are chaotic: the
 fp32 and fp64 trajectories of the SAME inputs then differ by O(1)
-(profiles/r02_calibration/: config 3 at 0.51 of nominal, growth 501x, fp32 vs
+(profiles/r02/calibration/: config 3 at 0.51 of nominal, growth 501x, fp32 vs
 fp64 final image 67% apart; config 4 at 0.8, growth 243x, 95% apart), so no fp32
 implementation can match an fp64 oracle there.  The calibration therefore
 bisects each pair's momentum scale for the largest value at which
