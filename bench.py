@@ -56,8 +56,9 @@ def parse():
                    help="pair groups on concurrent streams (default 2 for 2D batches >= 8)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
-    p.add_argument("--e2e-chunks", type=int, default=None,
-                   help="pair groups of the host-buffer pipeline (default: the API's choice)")
+    p.add_argument("--e2e-chunks", type=str, default=None,
+                   help="pair groups of the host-buffer pipeline: a count or comma-separated "
+                        "group sizes (default: the API's choice)")
     p.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     p.add_argument("--mu", type=float, default=None,
                    help="override the config's metamorphosis weight (e.g. --config 5 --mu 0)")
@@ -311,7 +312,7 @@ def run_ours(args):
             "avg_launch_ms": kt[dom],
             "share_of_step": share[dom],
             "traffic": kernel_traffic(dom),
-            "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/r01_traffic.json)",
+            "traffic_unit": "bytes per launch (dram read+write, ncu --set full, profiles/r02_traffic.json)",
         },
         "step_roofline": {
             "alg_bytes_per_voxel_step": sum(ab.values()),
@@ -338,15 +339,15 @@ def run_ours(args):
 
 
 # kernels each bench operation launches (split FIR operations are two kernels)
-NCU_NAMES = {"velocity": ("k_velocity2d_h<", "k_fir_axis0_f32<24, 0, 1>"),
-             "velocity_adjoint": ("k_fir_axis0_f32<24, 1, 0>", "k_velocity_adj2d_h<"),
+NCU_NAMES = {"velocity": ("k_vel_a<", "k_vel_b<"),
+             "velocity_adjoint": ("k_fir_axis0_f32p<24, 1, 0>", "k_velocity_adj2d_h<"),
              "sl_adjoint": ("k_sl_adjoint2d_tma",), "sl_step": ("k_sl_step2d_tma",)}
 
 
 def kernel_traffic(kernel: str):
     """DRAM bytes per launch of a bench kernel from the committed ncu capture."""
     try:
-        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(REPO, "profiles", "r02_traffic.json")) as f:
             tr = json.load(f)
     except Exception:
         return None
@@ -418,9 +419,12 @@ def run_e2e(c, args, dtype, world):
     z0 = torch.as_tensor(c.z0, dtype=dtype).pin_memory()
     stream = torch.cuda.current_stream()
 
+    chunks = args.e2e_chunks
+    if chunks is not None:
+        chunks = [int(n) for n in chunks.split(",")] if "," in chunks else int(chunks)
+
     def step():
-        zbar, terms, _ = mr.cost_and_grad_batch(src, tgt, z0, cfg, c.lam, c.rho,
-                                                chunks=args.e2e_chunks)
+        zbar, terms, _ = mr.cost_and_grad_batch(src, tgt, z0, cfg, c.lam, c.rho, chunks=chunks)
         return zbar, terms
 
     steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 10))

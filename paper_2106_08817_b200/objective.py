@@ -209,7 +209,14 @@ def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunk
         raise FieldError("source/target/z0 batch shapes differ")
     if chunks is None:
         chunks = 4 if B >= 16 else (2 if B >= 2 else 1)
-    chunks = max(1, min(int(chunks), B))
+    if isinstance(chunks, (list, tuple)):  # explicit group sizes (sum = B)
+        sizes = [int(n) for n in chunks]
+        if sum(sizes) != B or min(sizes) < 1:
+            raise FieldError(f"chunk sizes {sizes} do not partition the batch of {B}")
+    else:
+        chunks = max(1, min(int(chunks), B))
+        sizes = [B * (g + 1) // chunks - B * g // chunks for g in range(chunks)]
+    chunks = len(sizes)
     dtype = cfg.dtype if z0.dtype not in (torch.float32, torch.float64) else z0.dtype
     device = torch.device("cuda", torch.cuda.current_device())
 
@@ -223,7 +230,10 @@ def _host_pipeline(source, target, z0, cfg, lam, rho, raise_on_divergence, chunk
     guard_h = torch.empty((B, cfg.n_steps + 1), dtype=torch.int32, pin_memory=True)
     up, streams = _pipe_streams(device, chunks)
     up.wait_stream(torch.cuda.current_stream(device))
-    bounds = [(B * g // chunks, B * (g + 1) // chunks) for g in range(chunks)]
+    edges = [0]
+    for n in sizes:
+        edges.append(edges[-1] + n)
+    bounds = list(zip(edges[:-1], edges[1:]))
 
     trajs, tgts, ev_in, ev_J = [], [], [], []
     for g, (a, b) in enumerate(bounds):

@@ -76,3 +76,16 @@ def test_initial_divergence_raises_like_the_reference():
     with pytest.raises(mr.IntegrationDiverged):
         mr.optimize_batch(torch.as_tensor(src), torch.as_tensor(tgt), torch.as_tensor(z0), cfg, lam,
                           rho, mr.OptimizeConfig(max_iters=1))
+
+
+def test_host_pipeline_with_explicit_group_sizes_equals_the_device_call():
+    """cost_and_grad_batch on host tensors, pair groups given as sizes (objective._host_pipeline)."""
+    mr, cfg, lam, rho, src, tgt, z0 = _problem_set(4, torch.float64)
+    args = [torch.as_tensor(a) for a in (src, tgt, z0)]
+    zb_h, terms_h, guard_h = mr.cost_and_grad_batch(*args, cfg, lam, rho, chunks=[1, 3])
+    zb_d, terms_d, guard_d = mr.cost_and_grad_batch(*[a.cuda() for a in args], cfg, lam, rho)
+    assert not zb_h.is_cuda
+    assert torch.equal(zb_h, zb_d.cpu()) and torch.equal(terms_h, terms_d.cpu())
+    assert torch.equal(guard_h, guard_d.cpu())
+    with pytest.raises(mr.FieldError):
+        mr.cost_and_grad_batch(*args, cfg, lam, rho, chunks=[2, 3])
