@@ -162,6 +162,31 @@ def ops_case():
     np.savez_compressed(os.path.join(HERE, "ops.npz"), **out)
 
 
+def lddmm_case():
+    """The reference's SEPARATE deformation-only path, shoot_lddmm (integrator.py:222-277),
+    on a config whose mu is non-zero (it must be ignored), plus shoot() at mu = 0 on the
+    same inputs: the reference keeps them bitwise equal (acceptance criterion 2)."""
+    from morphreg import shoot_lddmm
+
+    src, _, z0 = instance((40, 33), 4, 1.0)
+    geom = GridGeometry(40, 33)
+    kern = GaussianKernel(1.5)
+    a = shoot_lddmm(ScalarField(geom, src), ScalarField(geom, z0),
+                    ShootingConfig(Scheme.SEMI_LAGRANGIAN, 8, 0.7, kern))
+    b = shoot(ScalarField(geom, src), ScalarField(geom, z0),
+              ShootingConfig(Scheme.SEMI_LAGRANGIAN, 8, 0.0, kern))
+    same = all(x.image.values.tobytes() == y.image.values.tobytes() and
+               x.momentum.values.tobytes() == y.momentum.values.tobytes()
+               for x, y in zip(a.states, b.states))
+    np.savez_compressed(os.path.join(HERE, "lddmm_path.npz"), source=src, z0=z0, n_steps=8,
+                        sigma=1.5, weights=kern.weights, mu_in_config=0.7,
+                        I=np.stack([s.image.values for s in a.states]),
+                        z=np.stack([s.momentum.values for s in a.states]),
+                        v=np.stack([cf(s.velocity.values) for s in a.states]),
+                        phi=cf(a.deformation.coords), reference_paths_bitwise_equal=same)
+    print("lddmm path: reference shoot_lddmm == shoot(mu=0) bitwise:", same)
+
+
 def guard_case():
     """A momentum that diverges: record (step, what) of IntegrationDiverged."""
     src, tgt, z0 = instance((16, 16), 2, 1.0)
@@ -213,8 +238,12 @@ def config1_case():
 
 if __name__ == "__main__":
     print("reference morphreg", morphreg.__version__, "numpy", np.__version__)
+    if "--only-lddmm" in sys.argv:
+        lddmm_case()
+        sys.exit(0)
     ops_case()
     guard_case()
+    lddmm_case()
     for case in SHOOT_CASES:
         shoot_case(*case)
     for name, scheme, *rest in SCHEME_CASES:

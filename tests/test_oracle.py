@@ -161,3 +161,14 @@ def test_oracle_3d_gradient_finite_differences():
     cm = O.cost(src, tgt, z0 - eps * d, lam, rho, T, mu, w)[0]
     fd = (cp - cm) / (2 * eps)
     assert float(np.sum(g * d)) == pytest.approx(fd, rel=1e-6)
+
+
+def test_oracle_mu_zero_equals_reference_lddmm_path():
+    """The reference's separate shoot_lddmm routine (integrator.py:222-277) on a config with
+    mu = 0.7: the oracle's shoot at mu = 0 reproduces every state bitwise."""
+    g = load_golden("lddmm_path.npz")
+    I, z, v, phi = O.shoot(g["source"], g["z0"], int(g["n_steps"]), 0.0, g["weights"], with_phi=True)
+    assert np.array_equal(np.stack(I), g["I"])
+    assert np.array_equal(np.stack(z), g["z"])
+    assert np.array_equal(np.stack(v), g["v"])
+    assert np.array_equal(phi, g["phi"])

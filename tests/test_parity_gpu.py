@@ -170,14 +170,28 @@ def test_zero_momentum_is_bitwise_identity(dtype):
     assert np.array_equal(traj.deformation.coords, ident)
 
 
-def test_mu_zero_matches_lddmm_path_bitwise():
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-13), (torch.float32, 1e-5)], ids=["fp64", "fp32"])
+def test_shoot_lddmm_matches_the_references_separate_lddmm_path(dtype, tol):
+    """shoot_lddmm against the golden of the REFERENCE's own deformation-only routine
+    (integrator.py:222-277, a code path of its own there), run on a config whose mu is
+    non-zero: mu must be ignored.  The device shoot(mu = 0) must then equal
+    shoot_lddmm bitwise, as the reference's two paths do (its acceptance criterion 2)."""
     import paper_2106_08817_b200 as mr
 
-    g = load_golden("shoot_E_40x33.npz")
-    cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, 8, 0.0, mr.GaussianKernel(1.5))
+    g = load_golden("lddmm_path.npz")
+    assert bool(g["reference_paths_bitwise_equal"])
+    kern = mr.GaussianKernel(float(g["sigma"]))
+    assert np.array_equal(kern.weights, g["weights"])
     src, z0 = mr.ScalarField.from_array(g["source"]), mr.ScalarField.from_array(g["z0"])
-    a = mr.shoot(src, z0, cfg)
-    b = mr.shoot_lddmm(src, z0, mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, 8, 0.7, cfg.kernel))
+    T = int(g["n_steps"])
+    b = mr.shoot_lddmm(src, z0, mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, T,
+                                                 float(g["mu_in_config"]), kern, dtype=dtype))
+    for k, st in enumerate(b.states):
+        assert rel_l2(st.image.values, g["I"][k]) < tol
+        assert rel_l2(st.momentum.values, g["z"][k]) < tol
+        assert rel_l2(np.moveaxis(st.velocity.values, -1, 0), g["v"][k]) < tol
+    assert rel_l2(np.moveaxis(b.deformation.coords, -1, 0), g["phi"]) < tol
+    a = mr.shoot(src, z0, mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, T, 0.0, kern, dtype=dtype))
     for sa, sb in zip(a.states, b.states):
         assert sa.image.values.tobytes() == sb.image.values.tobytes()
         assert sa.momentum.values.tobytes() == sb.momentum.values.tobytes()
