@@ -54,6 +54,9 @@ def parse():
                    help="shooting scheme (2D configs; the hot path is semi-lagrangian)")
     p.add_argument("--groups", type=int, default=None,
                    help="pair groups on concurrent streams (default 2 for 2D batches >= 8)")
+    p.add_argument("--shard-of", type=int, default=None,
+                   help="builder aid: time rank 0's shard of a W-rank job on this one GPU "
+                        "(no process group; predicts the per-rank step of --gpus W)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--e2e-chunks", type=str, default=None,
@@ -190,6 +193,8 @@ def run_ours(args):
     spec = CONFIGS[args.config]
     B_global = spec["batch"]
     pairs = shard(B_global, rank, world)
+    if args.shard_of and world == 1:
+        pairs = shard(B_global, 0, args.shard_of)
     c = make_config(args.config, pairs=pairs, mu=args.mu)
     d = len(c.shape)
     if d == 3 or args.scheme != "semi-lagrangian":
