@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 4)
 inline bool fast2d_ok(const Grid2& g, const void* p0, const void* p1, const void* p2,
                       const void* p3 = nullptr, const void* p4 = nullptr) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  return (g.W & 3) == 0 && (g.H & 1) == 0 && g.N < (1LL << 30) && al(p0) && al(p1) && al(p2) &&
+  return (g.W & 3) == 0 && (g.H & 1) == 0 && g.N < (1LL << 30) && g.B <= 65535 && al(p0) && al(p1) && al(p2) &&
          al(p3) && al(p4);
 }
 
