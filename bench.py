@@ -345,7 +345,7 @@ def run_ours(args):
 
 # kernels each bench operation launches (split FIR operations are two kernels)
 NCU_NAMES = {"velocity": ("k_vel_a<", "k_vel_b<"),
-             "velocity_adjoint": ("k_fir_axis0_f32p<24, 1, 0>", "k_velocity_adj2d_h<"),
+             "velocity_adjoint": ("k_fir_axis0_f32<24, 1, 0>", "k_velocity_adj2d_h<"),
              "sl_adjoint": ("k_sl_adjoint2d_tma",), "sl_step": ("k_sl_step2d_tma",)}
 
 

@@ -255,175 +255,10 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// ------------------------------------------------------------------------------
-// Persistent fp32 axis-0 FIR (same contract as k_fir_axis0_f32): one CTA per SM
-// slot walks a strided list of 64-column x kA0D-row tiles; the (kA0D + 2R)-row
-// region of tile i+1 arrives by TMA (zero fill outside [0, D) = the transpose's
-// zero padding) into the other half of a double buffer while tile i is filtered,
-// so the FMA pipe never waits for a cold load.  Forward border tiles copy the
-// clamped row into the zero-filled halo rows (replicate border, kernel.py:43-44).
-// ------------------------------------------------------------------------------
-template <int R>
-struct Ax0PSmem {
-  static constexpr int RD = kA0D + 2 * R;
-  static constexpr size_t buf = sizeof(float) * (size_t)RD * kA0X;  // multiple of 256 B
-  static constexpr size_t bytes = 128 + 2 * buf;
-};
-
-template <int R, bool TRANSPOSE, int EPI>
-__global__ void __launch_bounds__(kThreads)
-    k_fir_axis0_f32p(const __grid_constant__ CUtensorMap map, float* out, int D, long long HW,
-                     int V, int32_t* guard, int guard_stride, int ncomp, Taps<float> tp) {
-  using S = Ax0PSmem<R>;
-  constexpr int RD = S::RD;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  float* const buf0 = reinterpret_cast<float*>(smem_raw + 128);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nx = (int)((HW + kA0X - 1) / kA0X), nd = (D + kA0D - 1) / kA0D;
-  const long long ntiles = (long long)nx * nd * V;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](long long t, int slot) {
-    const int xb = (int)(t % nx);
-    const long long r = t / nx;
-    const int db = (int)(r % nd);
-    const int vol = (int)(r / nd);
-    mbar_expect_tx(&bar[slot], (unsigned)S::buf);
-    tma_load_3d(buf0 + slot * (S::buf / sizeof(float)), &map, xb * kA0X, db * kA0D - R, vol,
-                &bar[slot]);
-  };
-  if (tid == 0 && (long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-  const bool pair_ok = ((HW & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
-  int it = 0;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int slot = it & 1;
-    if (tid == 0 && t + gridDim.x < ntiles) {
-      // the other buffer was last read (and, at borders, written) by the generic
-      // proxy in the previous iteration, which ended with __syncthreads
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(t + gridDim.x, slot ^ 1);
-    }
-    const int xb = (int)(t % nx);
-    const long long r = t / nx;
-    const int db = (int)(r % nd);
-    const int vol = (int)(r / nd);
-    const int d_org = db * kA0D;
-    const long long x0 = (long long)xb * kA0X;
-    float* rgf = buf0 + slot * (S::buf / sizeof(float));
-    mbar_wait(&bar[slot], (unsigned)((it >> 1) & 1));
-    if (!TRANSPOSE && (d_org - R < 0 || d_org + kA0D + R > D)) {
-      // replicate border: halo rows outside [0, D) take the clamped row
-      for (int e = tid; e < RD * kA0X; e += kThreads) {
-        const int j = e / kA0X, c = e - j * kA0X;
-        const int gd = d_org - R + j;
-        if (gd < 0 || gd >= D) {
-          const int src = min(max(gd, 0), D - 1) - (d_org - R);
-          rgf[e] = rgf[src * kA0X + c];
-        }
-      }
-      __syncthreads();
-    }
-    const int i = 2 * lane;
-    const float2* s2 = reinterpret_cast<const float2*>(rgf + warp * kA0RB * kA0X + i);
-    float2 acc[kA0RB];
-#pragma unroll
-    for (int o = 0; o < kA0RB; ++o) acc[o] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int tt = 0; tt < kA0RB + 2 * R; ++tt) {
-      const float2 xv = s2[tt * (kA0X / 2)];
-#pragma unroll
-      for (int o = 0; o < kA0RB; ++o) {
-        const int tap = tt - o;
-        if (tap >= 0 && tap <= 2 * R) acc[o] = ffma2(xv, (float)tp.w[tap], acc[o]);
-      }
-    }
-    const int gd0 = d_org + warp * kA0RB;
-    const long long gx = x0 + i;
-    unsigned flags = 0;
-    if (gx < HW) {
-      float* p = out + (long long)vol * D * HW + (long long)gd0 * HW + gx;
-      const bool pair = pair_ok && gx + 1 < HW;
-#pragma unroll
-      for (int o = 0; o < kA0RB; ++o, p += HW) {
-        const int gd = gd0 + o;
-        if (gd < D) {
-          float2 val = acc[o];
-          if (EPI == 1) {
-            val = make_float2(-val.x, -val.y);
-            if (!(fabsf(val.x) <= 1e6f && fabsf(val.y) <= 1e6f)) {
-              flags |= guard_bits(val.x, MR_GUARD_VELOCITY_NONFINITE);
-              if (gx + 1 < HW) flags |= guard_bits(val.y, MR_GUARD_VELOCITY_NONFINITE);
-            }
-          }
-          if (pair) {
-            *reinterpret_cast<float2*>(p) = val;
-          } else {
-            p[0] = val.x;
-            if (gx + 1 < HW) p[1] = val.y;
-          }
-        }
-      }
-    }
-    if (EPI == 1 && guard && flags)
-      atomicOr(reinterpret_cast<int*>(guard + (long long)(vol / ncomp) * guard_stride), (int)flags);
-    if (TRANSPOSE && gx < HW) {
-      // edge rows 0 and n-1 of the transpose (cumulative-weight taps)
-      float* p = out + (long long)vol * D * HW + gx;
-      const bool pair = pair_ok && gx + 1 < HW;
-      auto put = [&](int gd, float2 val) {
-        float* q = p + (long long)gd * HW;
-        if (pair) {
-          *reinterpret_cast<float2*>(q) = val;
-        } else {
-          q[0] = val.x;
-          if (gx + 1 < HW) q[1] = val.y;
-        }
-      };
-      if (gd0 <= 0 && gd0 + kA0RB > 0) {
-        const int o = -gd0;
-        float2 a2 = make_float2(0.f, 0.f);
-#pragma unroll 1
-        for (int dd = 0; dd <= R; ++dd)
-          a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R - dd], a2);
-        put(0, a2);
-      }
-      if (gd0 <= D - 1 && gd0 + kA0RB > D - 1) {
-        const int o = D - 1 - gd0;
-        float2 a2 = make_float2(0.f, 0.f);
-#pragma unroll 1
-        for (int dd = -R; dd <= 0; ++dd)
-          a2 = ffma2(s2[(o + R + dd) * (kA0X / 2)], (float)tp.e[R + dd], a2);
-        put(D - 1, a2);
-      }
-    }
-    __syncthreads();  // every warp is done with this buffer before it is refilled
-  }
-}
-
-
 template <typename T, int R, bool TR, int EPI>
 int fir_axis0_r(const Taps<T>& tp, const T* in, T* out, int V, int D, long long HW,
                 int32_t* guard, int guard_stride, int ncomp, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {  // fp32: FFMA2 engine, 64-column x kA0D-row tiles
-    {  // persistent TMA double-buffered variant when the layout is TMA-describable
-      using P = Ax0PSmem<R>;
-      CUtensorMap map;
-      static const bool classic = getenv("MR_AX0_CLASSIC") != nullptr;  // A/B switch
-      if (!classic && HW <= INT_MAX && make_map3<float>(&map, in, (int)HW, D, V, kA0X, P::RD)) {
-        const cudaError_t attr = ensure_smem<k_fir_axis0_f32p<R, TR, EPI>>(P::bytes);
-        if (attr != cudaSuccess) return cuda_status(attr);
-        const long long ntiles = ((HW + kA0X - 1) / kA0X) * (long long)((D + kA0D - 1) / kA0D) * V;
-        const int ctas = persistent_ctas(k_fir_axis0_f32p<R, TR, EPI>, P::bytes, ntiles);
-        k_fir_axis0_f32p<R, TR, EPI><<<ctas, kThreads, P::bytes, s>>>(
-            map, out, D, HW, V, guard, guard_stride, ncomp, tp);
-        return cuda_status(cudaGetLastError());
-      }
-    }
     constexpr size_t bytes = Ax0F32Smem<R>::bytes;
     const cudaError_t attr = ensure_smem<k_fir_axis0_f32<R, TR, EPI>>(bytes);
     if (attr != cudaSuccess) return cuda_status(attr);

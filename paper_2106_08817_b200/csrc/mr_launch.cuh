@@ -21,25 +21,6 @@ inline int cuda_status(cudaError_t e) {
   return MR_ECUDA;
 }
 
-// Grid of a persistent kernel: resident CTAs per SM (occupancy of `kernel` at
-// `smem` bytes, capped by MR_PERSIST_CTAS_PER_SM when set) x SMs, at most `work`.
-template <typename K>
-inline int persistent_ctas(K kernel, size_t smem, long long work) {
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem) != cudaSuccess ||
-      per < 1)
-    per = 1;
-  static const int cap = [] {
-    const char* e = getenv("MR_PERSIST_CTAS_PER_SM");
-    return e ? atoi(e) : 0;
-  }();
-  if (cap > 0 && per > cap) per = cap;
-  const long long n = (long long)sms * per;
-  return (int)(work < n ? (work < 1 ? 1 : work) : n);
-}
-
 template <typename T>
 int launch_velocity2d(const Grid2& g, int R, const Taps<T>& tp, const T* I, const T* z, T* v,
                       int32_t* guard, int guard_stride, cudaStream_t s, T* vtmp = nullptr);
