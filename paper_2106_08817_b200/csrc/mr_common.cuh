@@ -103,6 +103,12 @@ __device__ __forceinline__ AxisPlan<float> plan_axis<float>(int pos, float vel, 
   const int fl = min(max(__float2int_rd(d), -(1 << 24)), 1 << 24);
   const float fr = d - (float)fl;
   const int ii = pos + fl;
+  if ((unsigned)(ii - 1) < (unsigned)(n - 2)) {  // 1 <= ii <= n - 2: the common case, no clamp
+    p.i0 = ii;
+    p.f = fr;
+    p.inside = true;
+    return p;
+  }
   const bool lo = ii < 0 || (ii == 0 && fr == 0.0f);
   const bool hi = ii >= n - 1;
   p.i0 = lo ? 0 : (hi ? n - 2 : ii);

@@ -66,27 +66,32 @@ __global__ void __launch_bounds__(kThreads)
 
   const T* __restrict__ I = a.I + b * N;
   const T* __restrict__ z = a.z + b * N;
+  T* __restrict__ In_b = a.In + b * N;  // per-pair bases: 32-bit pixel offsets below (N < 2^31)
+  T* __restrict__ zn_b = a.zn + b * N;
   unsigned fin = 0, fout = 0;
   constexpr int CPR = TX / 32;  // column chunks per row
+  // every tile pixel inside the image and at least 1 away from its edges: central
+  // differences only, no per-pixel border selects (same operations, bitwise equal)
+  const bool interior = y0 >= 1 && y0 + TY <= H - 1 && x0 >= 1 && x0 + TX <= W - 1;
 #pragma unroll
   for (int k = 0; k < C::PIX; ++k) {
     const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
     const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
     const int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) continue;
-    const long long q = (long long)y * W + x;
+    if (!interior && (x >= W || y >= H)) continue;
+    const int q = y * W + x;
     const int vi = (ty + 1) * VX + tx + 1;
     const T vy = sv0[vi], vx = sv1[vi];
     const AxisPlan<T> py = plan_axis<T>(y, vy, a.dt, H);
     const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
     const int ry = py.i0 - gy0, rx = px.i0 - gx0;  // window coords of corner 00
     T ia, ib2, ic, id, za, zb2, zc, zd;
-    if (ry >= 0 && ry + 1 < C::GY && rx >= 0 && rx + 1 < TX + 2 * HB) {
+    if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
       const int e = ry * GX + rx;
       ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
       za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
     } else {  // long back-trace: outside the staged window
-      const long long c00 = (long long)py.i0 * W + px.i0;
+      const int c00 = py.i0 * W + px.i0;
       ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
       za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
     }
@@ -98,15 +103,22 @@ __global__ void __launch_bounds__(kThreads)
     T bi = bilerp(ia, ib2, ic, id, py.f, px.f);
     if (a.has_mu) bi = bi + a.dtmu * sz[ce];  // advect_image_sl_arr: + dt*mu*z
     const T bz = bilerp(za, zb2, zc, zd, py.f, px.f);
-    const T up = (y > 0) ? sv0[vi - VX] : vy;
-    const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
-    const T lf = (x > 0) ? sv1[vi - 1] : vx;
-    const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
-    const T div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);  // fields.py:169-170
+    T div;  // fields.py:169-170
+    if (interior) {
+      div = (sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2);
+    } else {
+      const T up = (y > 0) ? sv0[vi - VX] : vy;
+      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+      const T lf = (x > 0) ? sv1[vi - 1] : vx;
+      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+      div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
+    }
     const T zn = bz * (T(1) - a.dt * div);
-    a.In[b * N + q] = bi;
-    a.zn[b * N + q] = zn;
-    fout |= guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) | guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+    In_b[q] = bi;
+    zn_b[q] = zn;
+    // guard: one comparison per output on the common path (NaN fails it too)
+    if (!(fabs(bi) <= T(1e6)) || !(fabs(zn) <= T(1e6)))
+      fout |= guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) | guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
     if (a.phi_in) {
       const long long c00 = (long long)py.i0 * W + px.i0;
 #pragma unroll
@@ -146,27 +158,38 @@ struct AdjCfg {
   static constexpr size_t bytes = C::head + sizeof(T) * (size_t)(2 * nG + 4 * nV + nS);
 };
 
-// 32-bit-key variant of scatter4_merged (cell index within one pair < 2^31)
+// Warp-merged scatter (scatter4_merged) with 32-bit keys (cell index within one pair < 2^31).
+// Two fields scattered through the same four cells (ibar and the weighted zbar share the
+// plan): one pair of key shuffles and one set of merge decisions for both.
 template <typename T>
-__device__ __forceinline__ void scatter4_merged32(T* __restrict__ out, int cell, bool valid, int W,
-                                                  T ca, T cb, T cc, T cd) {
+__device__ __forceinline__ void scatter4x2_merged32(T* __restrict__ out0, T* __restrict__ out1, int cell,
+                                                    bool valid, int W, T wa, T wb, T wc, T wd, T s0,
+                                                    T s1) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int key = valid ? cell : -4;
   const int prev_key = __shfl_up_sync(full, key, 1);
   const int next_key = __shfl_down_sync(full, key, 1);
-  const T pc = __shfl_up_sync(full, cc, 1);
-  const T pd = __shfl_up_sync(full, cd, 1);
+  T a0 = wa * s0, b0 = wb * s0, a1 = wa * s1, b1 = wb * s1;
+  const T c0 = wc * s0, d0 = wd * s0, c1 = wc * s1, d1 = wd * s1;
+  const T pc0 = __shfl_up_sync(full, c0, 1), pd0 = __shfl_up_sync(full, d0, 1);
+  const T pc1 = __shfl_up_sync(full, c1, 1), pd1 = __shfl_up_sync(full, d1, 1);
   if (!valid) return;
   if (lane > 0 && prev_key >= 0 && prev_key + 1 == key) {
-    ca += pc;
-    cb += pd;
+    a0 += pc0;
+    b0 += pd0;
+    a1 += pc1;
+    b1 += pd1;
   }
-  atomicAdd(out + cell, ca);
-  atomicAdd(out + cell + W, cb);
+  atomicAdd(out0 + cell, a0);
+  atomicAdd(out0 + cell + W, b0);
+  atomicAdd(out1 + cell, a1);
+  atomicAdd(out1 + cell + W, b1);
   if (!(lane < 31 && next_key >= 0 && key + 1 == next_key)) {
-    atomicAdd(out + cell + 1, cc);
-    atomicAdd(out + cell + W + 1, cd);
+    atomicAdd(out0 + cell + 1, c0);
+    atomicAdd(out0 + cell + W + 1, d0);
+    atomicAdd(out1 + cell + 1, c1);
+    atomicAdd(out1 + cell + W + 1, d1);
   }
 }
 
@@ -268,9 +291,17 @@ __global__ void __launch_bounds__(kThreads)
     const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
     T ia = T(0), ib2 = T(0), ic = T(0), id = T(0);
     T za = T(0), zb2 = T(0), zc = T(0), zd = T(0);
-    if (own) {
-      corners(sz, z, py, px, za, zb2, zc, zd);
-      corners(sI, I, py, px, ia, ib2, ic, id);
+    if (own) {  // both fields through one window test (same foot)
+      const int ry = py.i0 - gy0, rx = px.i0 - gx0;
+      if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
+        const int e = ry * GX + rx;
+        za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
+        ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
+      } else {
+        const int c00 = py.i0 * W + px.i0;
+        za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
+        ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
+      }
     }
     const T ib_ = sib[vi], zb_ = szb[vi];
     T scale = T(1);
@@ -287,9 +318,7 @@ __global__ void __launch_bounds__(kThreads)
     s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * (wy * wx * za + fy * wx * zb2 + wy * fx * zc + fy * fx * zd)) : T(0);
     const T wz = zb_ * scale;
     const int c00 = py.i0 * W + px.i0;
-    scatter4_merged32(ibo, c00, own, W, wy * wx * ib_, fy * wx * ib_, wy * fx * ib_,
-                      fy * fx * ib_);
-    scatter4_merged32(zbo, c00, own, W, wy * wx * wz, fy * wx * wz, wy * fx * wz, fy * fx * wz);
+    scatter4x2_merged32(ibo, zbo, c00, own, W, wy * wx, fy * wx, wy * fx, fy * fx, ib_, wz);
     if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
     // vbar = -dt (d/dy, d/dx)[P I] ibar - dt (d/dy, d/dx)[P z] w  (objective.py:131-132,143-145)
     const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
