@@ -10,6 +10,8 @@
 
 #include "mr_kernels2d.cuh"
 
+#include <type_traits>
+
 namespace mr {
 
 template <typename T>
@@ -273,98 +275,105 @@ __global__ void __launch_bounds__(kThreads)
     s_div[j * SX + i] = sv;
   }
 
-  // ---- phase 1: per owner pixel the plans, corners, scatters, s, and the partial
-  //      vbar (coordinate-gradient terms) kept in registers for phase 2 ----
-  T* __restrict__ ibo = a.ib + b * N;
-  T* __restrict__ zbo = a.zb + b * N;
-  constexpr int CPR = TX / 32;
-  T vbp0[C::PIX], vbp1[C::PIX];
-#pragma unroll
-  for (int k = 0; k < C::PIX; ++k) {
-    const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
-    const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
-    const int x = x0 + tx, y = y0 + ty;
-    const bool own = x < W && y < H;
-    const int vi = (ty + 1) * VX + tx + 1;
-    const T vy = sv0[vi], vx = sv1[vi];
-    const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
-    const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
-    T ia = T(0), ib2 = T(0), ic = T(0), id = T(0);
-    T za = T(0), zb2 = T(0), zc = T(0), zd = T(0);
-    if (own) {  // both fields through one window test (same foot)
-      const int ry = py.i0 - gy0, rx = px.i0 - gx0;
-      if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
-        const int e = ry * GX + rx;
-        za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
-        ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
-      } else {
-        const int c00 = py.i0 * W + px.i0;
-        za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
-        ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
+  // The two sweeps over the tile's pixels, specialised at compile time on `interior`
+  // (block-uniform): interior tiles carry no ownership predicates and no border stencils.
+  auto sweeps = [&](auto interior_tag) {
+    constexpr bool INT = decltype(interior_tag)::value;
+    // ---- phase 1: per owner pixel the plans, corners, scatters, s, and the partial
+    //      vbar (coordinate-gradient terms) kept in registers for phase 2 ----
+    T* __restrict__ ibo = a.ib + b * N;
+    T* __restrict__ zbo = a.zb + b * N;
+    constexpr int CPR = TX / 32;
+    T vbp0[C::PIX], vbp1[C::PIX];
+  #pragma unroll
+    for (int k = 0; k < C::PIX; ++k) {
+      const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
+      const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
+      const int x = x0 + tx, y = y0 + ty;
+      const bool own = INT || (x < W && y < H);
+      const int vi = (ty + 1) * VX + tx + 1;
+      const T vy = sv0[vi], vx = sv1[vi];
+      const AxisPlan<T> py = plan_axis<T>(own ? y : 0, vy, dt, H);
+      const AxisPlan<T> px = plan_axis<T>(own ? x : 0, vx, dt, W);
+      T ia = T(0), ib2 = T(0), ic = T(0), id = T(0);
+      T za = T(0), zb2 = T(0), zc = T(0), zd = T(0);
+      if (own) {  // both fields through one window test (same foot)
+        const int ry = py.i0 - gy0, rx = px.i0 - gx0;
+        if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
+          const int e = ry * GX + rx;
+          za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
+          ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
+        } else {
+          const int c00 = py.i0 * W + px.i0;
+          za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
+          ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
+        }
       }
+      const T ib_ = sib[vi], zb_ = szb[vi];
+      T scale = T(1);
+      if (INT) {
+        scale = T(1) - dt * ((sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2));
+      } else if (own) {
+        const T up = (y > 0) ? sv0[vi - VX] : vy;
+        const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+        const T lf = (x > 0) ? sv1[vi - 1] : vx;
+        const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+        scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
+      }
+      const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
+      s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * (wy * wx * za + fy * wx * zb2 + wy * fx * zc + fy * fx * zd)) : T(0);
+      const T wz = zb_ * scale;
+      const int c00 = py.i0 * W + px.i0;
+      scatter4x2_merged32(ibo, zbo, c00, own, W, wy * wx, fy * wx, wy * fx, fy * fx, ib_, wz);
+      if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
+      // vbar = -dt (d/dy, d/dx)[P I] ibar - dt (d/dy, d/dx)[P z] w  (objective.py:131-132,143-145)
+      const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
+      const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
+      const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
+      const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
+      vbp0[k] = -dt * ddy * ib_ + -dt * dzy * wz;
+      vbp1[k] = -dt * ddx * ib_ + -dt * dzx * wz;
     }
-    const T ib_ = sib[vi], zb_ = szb[vi];
-    T scale = T(1);
-    if (interior) {
-      scale = T(1) - dt * ((sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2));
-    } else if (own) {
-      const T up = (y > 0) ? sv0[vi - VX] : vy;
-      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
-      const T lf = (x > 0) ? sv1[vi - 1] : vx;
-      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
-      scale = T(1) - dt * (grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W));
-    }
-    const T fy = py.f, fx = px.f, wy = T(1) - fy, wx = T(1) - fx;
-    s_div[(ty + 1) * SX + tx + 1] = own ? -dt * (zb_ * (wy * wx * za + fy * wx * zb2 + wy * fx * zc + fy * fx * zd)) : T(0);
-    const T wz = zb_ * scale;
-    const int c00 = py.i0 * W + px.i0;
-    scatter4x2_merged32(ibo, zbo, c00, own, W, wy * wx, fy * wx, wy * fx, fy * fx, ib_, wz);
-    if (own && a.has_mu) atomicAdd(zbo + (long long)y * W + x, a.dtmu * ib_);  // :133
-    // vbar = -dt (d/dy, d/dx)[P I] ibar - dt (d/dy, d/dx)[P z] w  (objective.py:131-132,143-145)
-    const T ddy = (wx * (ib2 - ia) + fx * (id - ic)) * (py.inside ? T(1) : T(0));
-    const T ddx = (wy * (ic - ia) + fy * (id - ib2)) * (px.inside ? T(1) : T(0));
-    const T dzy = (wx * (zb2 - za) + fx * (zd - zc)) * (py.inside ? T(1) : T(0));
-    const T dzx = (wy * (zc - za) + fy * (zd - zb2)) * (px.inside ? T(1) : T(0));
-    vbp0[k] = -dt * ddy * ib_ + -dt * dzy * wz;
-    vbp1[k] = -dt * ddx * ib_ + -dt * dzx * wz;
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // ---- phase 2: vbar += D^T s (objective.py:146-147), then the k = 0 fold ----
-#pragma unroll
-  for (int k = 0; k < C::PIX; ++k) {
-    const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
-    const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
-    const int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) continue;
-    T vb0 = vbp0[k], vb1 = vbp1[k];
-    const int j = ty + 1, i = tx + 1;
-    const T sm_ = s_div[(j - 1) * SX + i], sp_ = s_div[(j + 1) * SX + i];
-    const T sl_ = s_div[j * SX + i - 1], sr_ = s_div[j * SX + i + 1];
-    if (interior) {  // D^T s = 0.5 s[j-1] - 0.5 s[j+1] away from the edges
-      vb0 += T(0.5) * sm_ - T(0.5) * sp_;
-      vb1 += T(0.5) * sl_ - T(0.5) * sr_;
-    } else {
-      const T s_first_y = (y <= 1) ? s_div[(j - y) * SX + i] : T(0);
-      const T s_last_y = (y >= H - 2) ? s_div[(j + (H - 1 - y)) * SX + i] : T(0);
-      vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
-      const T s_first_x = (x <= 1) ? s_div[j * SX + i - x] : T(0);
-      const T s_last_x = (x >= W - 2) ? s_div[j * SX + i + (W - 1 - x)] : T(0);
-      vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+    // ---- phase 2: vbar += D^T s (objective.py:146-147), then the k = 0 fold ----
+  #pragma unroll
+    for (int k = 0; k < C::PIX; ++k) {
+      const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
+      const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
+      const int x = x0 + tx, y = y0 + ty;
+      if (!INT && (x >= W || y >= H)) continue;
+      T vb0 = vbp0[k], vb1 = vbp1[k];
+      const int j = ty + 1, i = tx + 1;
+      const T sm_ = s_div[(j - 1) * SX + i], sp_ = s_div[(j + 1) * SX + i];
+      const T sl_ = s_div[j * SX + i - 1], sr_ = s_div[j * SX + i + 1];
+      if (INT) {  // D^T s = 0.5 s[j-1] - 0.5 s[j+1] away from the edges
+        vb0 += T(0.5) * sm_ - T(0.5) * sp_;
+        vb1 += T(0.5) * sl_ - T(0.5) * sr_;
+      } else {
+        const T s_first_y = (y <= 1) ? s_div[(j - y) * SX + i] : T(0);
+        const T s_last_y = (y >= H - 2) ? s_div[(j + (H - 1 - y)) * SX + i] : T(0);
+        vb0 += diff_adj1(sm_, sp_, s_first_y, s_last_y, y, H);
+        const T s_first_x = (x <= 1) ? s_div[j * SX + i - x] : T(0);
+        const T s_last_x = (x >= W - 2) ? s_div[j * SX + i + (W - 1 - x)] : T(0);
+        vb1 += diff_adj1(sl_, sr_, s_first_x, s_last_x, x, W);
+      }
+      const long long q = (long long)y * W + x;
+      if (a.reg_lam != T(0)) {  // k = 0: fold -lam*m0
+        const int ce = (ty + HB) * GX + tx + HB;
+        const T c = sI[ce];
+        const T g0 = grad1(sI[ce - GX], c, sI[ce + GX], y, H);
+        const T g1 = grad1(sI[ce - 1], c, sI[ce + 1], x, W);
+        const T zz = sz[ce];
+        vb0 = vb0 - a.reg_lam * (zz * g0);
+        vb1 = vb1 - a.reg_lam * (zz * g1);
+      }
+      a.vbar[b * 2 * N + q] = vb0;
+      a.vbar[b * 2 * N + N + q] = vb1;
     }
-    const long long q = (long long)y * W + x;
-    if (a.reg_lam != T(0)) {  // k = 0: fold -lam*m0
-      const int ce = (ty + HB) * GX + tx + HB;
-      const T c = sI[ce];
-      const T g0 = grad1(sI[ce - GX], c, sI[ce + GX], y, H);
-      const T g1 = grad1(sI[ce - 1], c, sI[ce + 1], x, W);
-      const T zz = sz[ce];
-      vb0 = vb0 - a.reg_lam * (zz * g0);
-      vb1 = vb1 - a.reg_lam * (zz * g1);
-    }
-    a.vbar[b * 2 * N + q] = vb0;
-    a.vbar[b * 2 * N + N + q] = vb1;
-  }
+  };
+  if (interior) sweeps(std::true_type{});
+  else sweeps(std::false_type{});
 }
 
 }  // namespace mr
