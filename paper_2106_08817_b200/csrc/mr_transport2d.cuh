@@ -75,61 +75,75 @@ __global__ void __launch_bounds__(kThreads)
   // every tile pixel inside the image and at least 1 away from its edges: central
   // differences only, no per-pixel border selects (same operations, bitwise equal)
   const bool interior = y0 >= 1 && y0 + TY <= H - 1 && x0 >= 1 && x0 + TX <= W - 1;
-#pragma unroll
-  for (int k = 0; k < C::PIX; ++k) {
-    const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
-    const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
-    const int x = x0 + tx, y = y0 + ty;
-    if (!interior && (x >= W || y >= H)) continue;
-    const int q = y * W + x;
-    const int vi = (ty + 1) * VX + tx + 1;
-    const T vy = sv0[vi], vx = sv1[vi];
-    const AxisPlan<T> py = plan_axis<T>(y, vy, a.dt, H);
-    const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
-    const int ry = py.i0 - gy0, rx = px.i0 - gx0;  // window coords of corner 00
-    T ia, ib2, ic, id, za, zb2, zc, zd;
-    if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
-      const int e = ry * GX + rx;
-      ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
-      za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
-    } else {  // long back-trace: outside the staged window
-      const int c00 = py.i0 * W + px.i0;
-      ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
-      za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
-    }
-    const int ce = (ty + HB) * GX + tx + HB;  // own pixel in the window
-    if (a.guard_in) {  // _guard(0, image, momentum) on the inputs (integrator.py:184)
-      fin |= guard_bits(sI[ce], MR_GUARD_IMAGE_NONFINITE) |
-             guard_bits(sz[ce], MR_GUARD_MOMENTUM_NONFINITE);
-    }
-    T bi = bilerp(ia, ib2, ic, id, py.f, px.f);
-    if (a.has_mu) bi = bi + a.dtmu * sz[ce];  // advect_image_sl_arr: + dt*mu*z
-    const T bz = bilerp(za, zb2, zc, zd, py.f, px.f);
-    T div;  // fields.py:169-170
-    if (interior) {
-      div = (sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2);
-    } else {
-      const T up = (y > 0) ? sv0[vi - VX] : vy;
-      const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
-      const T lf = (x > 0) ? sv1[vi - 1] : vx;
-      const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
-      div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
-    }
-    const T zn = bz * (T(1) - a.dt * div);
-    In_b[q] = bi;
-    zn_b[q] = zn;
-    // guard: one comparison per output on the common path (NaN fails it too)
-    if (!(fabs(bi) <= T(1e6)) || !(fabs(zn) <= T(1e6)))
-      fout |= guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) | guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
-    if (a.phi_in) {
-      const long long c00 = (long long)py.i0 * W + px.i0;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const T* __restrict__ ph = a.phi_in + (b * 2 + c) * N;
-        a.phi_out[(b * 2 + c) * N + q] =
-            bilerp(ph[c00], ph[c00 + W], ph[c00 + 1], ph[c00 + W + 1], py.f, px.f);
+  // the pixel loop, specialised at compile time on two block-uniform facts: `interior`
+  // and `plain` (no input guard, no deformation grid: every step but the first of a shoot
+  // without phi)
+  auto sweep = [&](auto interior_tag, auto plain_tag) {
+    constexpr bool INT = decltype(interior_tag)::value, PLAIN = decltype(plain_tag)::value;
+  #pragma unroll
+    for (int k = 0; k < C::PIX; ++k) {
+      const int tx = (threadIdx.x & 31) + 32 * (k % CPR);
+      const int ty = (threadIdx.x >> 5) + (k / CPR) * (kThreads / 32);
+      const int x = x0 + tx, y = y0 + ty;
+      if (!INT && (x >= W || y >= H)) continue;
+      const int q = y * W + x;
+      const int vi = (ty + 1) * VX + tx + 1;
+      const T vy = sv0[vi], vx = sv1[vi];
+      const AxisPlan<T> py = plan_axis<T>(y, vy, a.dt, H);
+      const AxisPlan<T> px = plan_axis<T>(x, vx, a.dt, W);
+      const int ry = py.i0 - gy0, rx = px.i0 - gx0;  // window coords of corner 00
+      T ia, ib2, ic, id, za, zb2, zc, zd;
+      if ((unsigned)ry < (unsigned)(C::GY - 1) && (unsigned)rx < (unsigned)(TX + 2 * HB - 1)) {
+        const int e = ry * GX + rx;
+        ia = sI[e]; ib2 = sI[e + GX]; ic = sI[e + 1]; id = sI[e + GX + 1];
+        za = sz[e]; zb2 = sz[e + GX]; zc = sz[e + 1]; zd = sz[e + GX + 1];
+      } else {  // long back-trace: outside the staged window
+        const int c00 = py.i0 * W + px.i0;
+        ia = I[c00]; ib2 = I[c00 + W]; ic = I[c00 + 1]; id = I[c00 + W + 1];
+        za = z[c00]; zb2 = z[c00 + W]; zc = z[c00 + 1]; zd = z[c00 + W + 1];
+      }
+      const int ce = (ty + HB) * GX + tx + HB;  // own pixel in the window
+      if (!PLAIN && a.guard_in) {  // _guard(0, image, momentum) on the inputs (integrator.py:184)
+        fin |= guard_bits(sI[ce], MR_GUARD_IMAGE_NONFINITE) |
+               guard_bits(sz[ce], MR_GUARD_MOMENTUM_NONFINITE);
+      }
+      T bi = bilerp(ia, ib2, ic, id, py.f, px.f);
+      if (a.has_mu) bi = bi + a.dtmu * sz[ce];  // advect_image_sl_arr: + dt*mu*z
+      const T bz = bilerp(za, zb2, zc, zd, py.f, px.f);
+      T div;  // fields.py:169-170
+      if (INT) {
+        div = (sv0[vi + VX] - sv0[vi - VX]) / T(2) + (sv1[vi + 1] - sv1[vi - 1]) / T(2);
+      } else {
+        const T up = (y > 0) ? sv0[vi - VX] : vy;
+        const T dn = (y < H - 1) ? sv0[vi + VX] : vy;
+        const T lf = (x > 0) ? sv1[vi - 1] : vx;
+        const T rt = (x < W - 1) ? sv1[vi + 1] : vx;
+        div = grad1(up, vy, dn, y, H) + grad1(lf, vx, rt, x, W);
+      }
+      const T zn = bz * (T(1) - a.dt * div);
+      In_b[q] = bi;
+      zn_b[q] = zn;
+      // guard: one comparison per output on the common path (NaN fails it too)
+      if (!(fabs(bi) <= T(1e6)) || !(fabs(zn) <= T(1e6)))
+        fout |= guard_bits(bi, MR_GUARD_IMAGE_NONFINITE) | guard_bits(zn, MR_GUARD_MOMENTUM_NONFINITE);
+      if (!PLAIN && a.phi_in) {
+        const long long c00 = (long long)py.i0 * W + px.i0;
+  #pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const T* __restrict__ ph = a.phi_in + (b * 2 + c) * N;
+          a.phi_out[(b * 2 + c) * N + q] =
+              bilerp(ph[c00], ph[c00 + W], ph[c00 + 1], ph[c00 + W + 1], py.f, px.f);
+        }
       }
     }
+  };
+  const bool plain = !a.guard_in && !a.phi_in;
+  if (interior) {
+    if (plain) sweep(std::true_type{}, std::true_type{});
+    else sweep(std::true_type{}, std::false_type{});
+  } else {
+    if (plain) sweep(std::false_type{}, std::true_type{});
+    else sweep(std::false_type{}, std::false_type{});
   }
   if (fin && a.guard_in)
     atomicOr(reinterpret_cast<int*>(a.guard_in + (long long)b * a.guard_stride), (int)fin);
