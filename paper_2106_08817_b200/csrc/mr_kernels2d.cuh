@@ -1510,7 +1510,53 @@ __global__ void __launch_bounds__(kThreads) k_cost_terms2d(CostArgs<T> a) {
   double data = 0.0, vn = 0.0, zn = 0.0;
   // warp <-> row, lanes <-> consecutive columns (no per-element index division)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // fp32 rows whose layout allows it: 4 consecutive pixels per lane, float4 loads, the
+  // row's loads issued together (the scalar loop below is latency-bound: one dependent
+  // round trip per 32 pixels)
+  bool vec = false;
+  if constexpr (sizeof(T) == 4) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    vec = (W & 3) == 0 && (N & 3) == 0 && al(a.I0) && al(a.z0) && al(a.v0) && al(a.IT) && al(a.J) &&
+          (!a.seed || al(a.seed));
+  }
   for (int y = blockIdx.x * kNW + warp; y < H; y += gridDim.x * kNW) {
+    if constexpr (sizeof(T) == 4) {
+      if (vec) {
+        const int row = y * W;
+        const int rup = (y > 0 ? y - 1 : y) * W, rdn = (y < H - 1 ? y + 1 : y) * W;
+        const float cgy = (y == 0 || y == H - 1) ? 1.f : 0.5f;  // one-sided rows: up / dn == c there
+#pragma unroll 4
+        for (int x = 4 * lane; x < W; x += 128) {
+          const float4 it = *reinterpret_cast<const float4*>(IT + row + x);
+          const float4 jj = *reinterpret_cast<const float4*>(J + row + x);
+          const float4 c = *reinterpret_cast<const float4*>(I0 + row + x);
+          const float4 up = *reinterpret_cast<const float4*>(I0 + rup + x);
+          const float4 dn = *reinterpret_cast<const float4*>(I0 + rdn + x);
+          const float4 zz = *reinterpret_cast<const float4*>(z0 + row + x);
+          const float4 wa = *reinterpret_cast<const float4*>(w0 + row + x);
+          const float4 wb = *reinterpret_cast<const float4*>(w0 + N + row + x);
+          const float lf = x > 0 ? I0[row + x - 1] : c.x, rt = x + 4 < W ? I0[row + x + 4] : c.w;
+          const float d4[4] = {it.x - jj.x, it.y - jj.y, it.z - jj.z, it.w - jj.w};
+          if (a.seed)
+            *reinterpret_cast<float4*>(a.seed + b * N + row + x) = make_float4(d4[0], d4[1], d4[2], d4[3]);
+          const float cv[6] = {lf, c.x, c.y, c.z, c.w, rt};
+          const float g0[4] = {(dn.x - up.x) * cgy, (dn.y - up.y) * cgy, (dn.z - up.z) * cgy,
+                               (dn.w - up.w) * cgy};
+          const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
+          const float av[4] = {wa.x, wa.y, wa.z, wa.w}, bv[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int gx = x + p;
+            const float g1 = gx == 0 ? cv[p + 2] - cv[p + 1]
+                                     : (gx == W - 1 ? cv[p + 1] - cv[p] : (cv[p + 2] - cv[p]) * 0.5f);
+            data += (double)d4[p] * (double)d4[p];
+            vn += (double)(zv[p] * g0[p]) * (double)av[p] + (double)(zv[p] * g1) * (double)bv[p];
+            zn += (double)zv[p] * (double)zv[p];
+          }
+        }
+        continue;
+      }
+    }
     for (int x = lane; x < W; x += 32) {
       const long long q = (long long)y * W + x;
       T diff = IT[q] - J[q];
