@@ -89,3 +89,32 @@ def test_host_pipeline_with_explicit_group_sizes_equals_the_device_call():
     assert torch.equal(guard_h, guard_d.cpu())
     with pytest.raises(mr.FieldError):
         mr.cost_and_grad_batch(*args, cfg, lam, rho, chunks=[2, 3])
+
+
+def test_batched_line_search_runs_in_3d_and_matches_single_pair_runs():
+    """optimize_batch is dimension-agnostic: two 3D pairs, each equal to its own run."""
+    import paper_2106_08817_b200 as mr
+
+    rng = np.random.default_rng(9)
+    shape = (12, 16, 20)
+    kern = mr.GaussianKernel(1.5)
+    cfg = mr.ShootingConfig(mr.Scheme.SEMI_LAGRANGIAN, 3, 0.2, kern, dtype=torch.float64)
+
+    src = rng.random((2,) + shape)
+    tgt = np.clip(src + 0.1 * rng.standard_normal((2,) + shape), 0, 1)
+    tgt[1] *= 2.0  # different contrast: different accepted steps
+    src[1] *= 2.0
+    z0 = np.zeros((2,) + shape)
+    ocfg = mr.OptimizeConfig(max_iters=3, init_step=50.0)
+    both = mr.optimize_batch(torch.as_tensor(src), torch.as_tensor(tgt), torch.as_tensor(z0), cfg,
+                             1e-2, 1.0, ocfg)
+    for b in range(2):
+        one = mr.optimize_batch(torch.as_tensor(src[b:b + 1]), torch.as_tensor(tgt[b:b + 1]),
+                                torch.as_tensor(z0[b:b + 1]), cfg, 1e-2, 1.0, ocfg)
+        assert both.terminations[b] == one.terminations[0]
+        assert both.step_sizes[b] == one.step_sizes[0]
+        assert [h.total for h in both.histories[b]] == pytest.approx(
+            [h.total for h in one.histories[0]], rel=1e-12)
+        assert torch.allclose(both.z0[b], one.z0[0], rtol=1e-10, atol=1e-14)
+        totals = [h.total for h in both.histories[b]]
+        assert len(totals) >= 2 and totals[-1] < totals[0]
