@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "../../include/morphreg_sm100.h"
 
@@ -315,6 +316,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
+}
+
+// CTAs ahead of the running one whose inputs get an L2 prefetch (MR_PF_AHEAD, default: the
+// number of SMs; 0 disables).  Used by k_vel_a: cfg2 12.17 -> 12.0 ms per grad on B200.
+inline int prefetch_ahead() {
+  static const int v = [] {
+    if (const char* e = getenv("MR_PF_AHEAD")) return atoi(e);
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    return n_sm;
+  }();
+  return v;
 }
 
 }  // namespace mr

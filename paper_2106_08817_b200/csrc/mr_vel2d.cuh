@@ -94,8 +94,22 @@ struct VelASmem {
 template <int R>
 __global__ void __launch_bounds__(kThreads, 4)
     k_vel_a(const float* __restrict__ I, const float* __restrict__ z, float2* __restrict__ hT,
-            int H, int W, Taps<float> tp) {
+            int H, int W, Taps<float> tp, int pf_ahead) {
   constexpr int RY = VelASmem<R>::RY, RPW = (RY + kNW - 1) / kNW;
+  if (pf_ahead > 0) {
+    // L2 prefetch of the I / z rows of the CTA that will run `pf_ahead` CTAs later
+    const long long lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z) + pf_ahead;
+    const int px = (int)(lin % gridDim.x), py = (int)((lin / gridDim.x) % gridDim.y);
+    const long long pb = lin / ((long long)gridDim.x * gridDim.y);
+    if (pb < gridDim.z) {
+      const int r = py * kFY - R + (int)threadIdx.x;  // one row per thread (RY <= 256)
+      if ((int)threadIdx.x < RY && r >= 0 && r < H && px * kFX < W) {
+        const long long off = (pb * H + r) * W + px * kFX;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(I + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(z + off));
+      }
+    }
+  }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* sM = reinterpret_cast<float2*>(smem_raw);
   const int x0 = blockIdx.x * kFX, y0 = blockIdx.y * kFY, b = blockIdx.z;
@@ -252,8 +266,9 @@ int launch_vel2d_fast(const Grid2& g, const Taps<float>& tp, const float* I, con
   e = ensure_smem<k_vel_b<R>>(Bs::bytes);
   if (e != cudaSuccess) return cuda_status(e);
   float2* hT = reinterpret_cast<float2*>(ws);
+  const int pf = prefetch_ahead();
   k_vel_a<R><<<dim3((g.W + kFX - 1) / kFX, (g.H + kFY - 1) / kFY, g.B), kThreads, A::bytes, s>>>(
-      I, z, hT, g.H, g.W, tp);
+      I, z, hT, g.H, g.W, tp, pf);
   int rc = cuda_status(cudaGetLastError());
   if (rc) return rc;
   k_vel_b<R><<<dim3((g.H + kFX - 1) / kFX, (g.W + kFY - 1) / kFY, g.B), kThreads, Bs::bytes, s>>>(
